@@ -1,0 +1,62 @@
+"""Build libpfgpu.so (sm_100a) in-tree with nvcc.
+
+pf_eval.cu is compiled with -fmad=false so its fp64 arithmetic rounds where
+the reference's wf1 rounds (see the file header); pf_plan.cu (symbolic build,
+C ABI) uses default flags.  Static cudart; the library exports only the
+extern "C" symbols of include/pfgpu.h.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT = PKG / "libpfgpu.so"
+BUILD = ROOT / "build"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+          "-I", str(ROOT / "include"), *ARCH]
+UNITS = {
+    "pf_eval.cu": ["-fmad=false"],
+    "pf_plan.cu": [],
+}
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (Path(cand).exists() or cand == "nvcc"):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    objs = []
+    deps = [CSRC / "pf_internal.cuh", ROOT / "include" / "pfgpu.h"]
+    for src, extra in UNITS.items():
+        s = CSRC / src
+        o = BUILD / (src + ".o")
+        objs.append(o)
+        newest = max(p.stat().st_mtime for p in [s, *deps])
+        if not force and o.exists() and o.stat().st_mtime >= newest:
+            continue
+        cmd = [nvcc(), *COMMON, *extra, "-Xptxas", "-v" if verbose else "-O3", "-c", str(s),
+               "-o", str(o)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    if force or not OUT.exists() or OUT.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(OUT), *map(str, objs), "-cudart", "static"]
+        subprocess.run(cmd, check=True)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
+    print(OUT)

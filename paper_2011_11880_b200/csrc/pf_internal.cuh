@@ -1,0 +1,116 @@
+// pf_internal.cuh - device plan layout shared by the libpfgpu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/pfgpu.h"
+
+namespace pf {
+
+// Per-incidence metadata flag bits (inc_meta.z).
+constexpr int32_t KSIDE = 1 << 30;   // this bus is the branch's k (to) terminal
+constexpr int32_t FIRST = 1 << 29;   // first incidence of this neighbour in the bus's list
+constexpr int32_t POS_MASK = (1 << 29) - 1;
+
+// Per-bus row descriptor (bus_row.w flag bit).
+constexpr int32_t VDIAG = 1 << 30;   // row holds a (g, V_i) diagonal entry
+
+// Device-list entry types, in the reference's pool-segment order (residual.py:57).
+enum DevType : int32_t { DEV_PQ = 0, DEV_PV = 1, DEV_SLACK = 2, DEV_SHUNT = 3 };
+
+// Everything the evaluation kernels read.  All pointers are device memory.
+struct DevicePlan {
+    int32_t N, L, P, G, S, H, n_gen, n_var, nnz, n_inc;
+    // incidence lists: bus i owns [inc_ptr[i], inc_ptr[i+1]) in the order
+    // (branches with h=i ascending) ++ (branches with k=i ascending)
+    const int32_t* inc_ptr;   // [N+1]
+    const int4* inc_meta;     // [n_inc] {neighbour j, branch l, pos|flags, 0}
+    const double4* inc_coef;  // [n_inc] {g1, b1, gs, bs}: h side {gl, bl, gsh, bsh},
+                              //          k side {gl2, -bl2, gsk, bsk}
+    const int4* bus_row;      // [N] {rp, rq, nb, pos_i|VDIAG}: CSR offsets of rows
+                              // g_p[i], g_q[i], theta-block size, diagonal rank
+    const int32_t* dev_ptr;   // [N+1]
+    const int4* dev_list;     // [n_dev] {type, index, jpos_a, jpos_b}
+    // device parameters (base values; scenarios may override P/Q)
+    const double *pq_p0, *pq_q0, *pv_p0, *pv_v0, *sl_v0, *sl_th0, *sh_g, *sh_b;
+    const int32_t *pv_qg, *sl_qg, *sl_ps;
+    const int32_t* gen_row_pos;  // [n_gen + S]: CSR position of the single entry of
+                                 // rows g_V (n_gen) then g_theta (S)
+    // original branch-indexed SoA (per-model entry points)
+    const int32_t *bus_h, *bus_k;
+    const double *gl, *bl, *gl2, *bl2, *gsh, *bsh, *gsk, *bsk;
+    const int32_t *pq_bus, *pv_bus, *sl_bus, *sh_bus;
+    // pattern
+    const int32_t* csr_indptr;   // [n_var+1]
+    const int32_t* csr_indices;  // [nnz]
+    const int32_t* csc_indptr;   // [n_var+1]
+    const int32_t* csc_indices;  // [nnz]
+    const int32_t* csc_perm;     // [nnz] csc value q = csr value csc_perm[q]
+};
+
+struct Staging {
+    int32_t n_streams = 0;
+    int32_t blocks = 0;           // scenario blocks per stage
+    cudaStream_t streams[8] = {};
+    double* y[8] = {};
+    double* g[8] = {};
+    double* j[8] = {};
+    double* pq_p[8] = {};
+    double* pq_q[8] = {};
+    double* pv_p[8] = {};
+    int32_t* outage[8] = {};
+    double* norms[8] = {};
+};
+
+}  // namespace pf
+
+struct pf_plan {
+    pf::DevicePlan d;
+    int32_t max_deg = 0;
+    void* owned[64] = {};   // device allocations to free
+    int n_owned = 0;
+    // single-grid host drop-in staging
+    double *s_y = nullptr, *s_g = nullptr, *s_j = nullptr, *s_jc = nullptr, *s_norm = nullptr;
+    cudaStream_t s_stream = nullptr;
+    pf::Staging batch;
+};
+
+namespace pf {
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+#define PF_CUDA(call)                                         \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return pf::cuda_fail(_e, #call); \
+    } while (0)
+
+// kernel launchers (pf_eval.cu)
+cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, double* j,
+                               double* norm, cudaStream_t st);
+cudaError_t launch_eval_batched(const DevicePlan& d, int32_t K, const double* y,
+                                const double* pq_p, const double* pq_q, const double* pv_p,
+                                const int32_t* outage, double* g, double* j, double* norms,
+                                cudaStream_t st);
+cudaError_t launch_jac_to_csc(const DevicePlan& d, int32_t K, const double* jcsr, double* jcsc,
+                              cudaStream_t st);
+cudaError_t launch_line_injections(const DevicePlan& d, const double* y, double* ph, double* pk,
+                                   double* qh, double* qk, cudaStream_t st);
+cudaError_t launch_line_jac_slots(const DevicePlan& d, const double* y, double* slots,
+                                  cudaStream_t st);
+cudaError_t launch_device_injections(const DevicePlan& d, const double* y, double* pool,
+                                     cudaStream_t st);
+cudaError_t launch_device_jac_slots(const DevicePlan& d, const double* y, double* slots,
+                                    cudaStream_t st);
+cudaError_t launch_join_rows(int32_t n, const int32_t* ptr, const int32_t* split,
+                             const int32_t* idx, const double* pool, double* out,
+                             cudaStream_t st);
+cudaError_t launch_gather_sum(int32_t n, const int32_t* ptr, const int32_t* idx,
+                              const double* vals, double* out, cudaStream_t st);
+
+}  // namespace pf

@@ -1,0 +1,323 @@
+"""GPU parity: libpfgpu (sm_100a) against the reference's golden vectors and
+the CPU oracle, through the C ABI.
+
+Criterion (BASELINE.json north star): Jacobian pattern bit-exact with the
+reference's; residual and Jacobian values per entry within
+max(1e-12 |ref|, 1e-14).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from _util import (SINGLE, assert_parity, csc_to_csr_perm, load, parity_failures, system_of)
+from paper_2011_11880_b200 import synth
+from paper_2011_11880_b200.system_model import build_system, random_state
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _plan(s):
+    from paper_2011_11880_b200.plan import Plan
+
+    return Plan(s)
+
+
+def _dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
+
+
+def _eval(plan, y):
+    g = plan.empty(plan.n_var)
+    j = plan.empty(plan.nnz)
+    n = plan.empty(1)
+    plan.eval(_dev(y), g, j, n)
+    torch.cuda.synchronize()
+    return g[: plan.n_var].cpu().numpy(), j[: plan.nnz].cpu().numpy(), float(n[0])
+
+
+@pytest.fixture(scope="module", params=SINGLE)
+def gfx(request):
+    d = load(request.param)
+    s = system_of(d)
+    return d, s, _plan(s)
+
+
+def test_pattern_bit_exact_vs_reference(gfx):
+    d, s, plan = gfx
+    indptr, indices = plan.pattern_csr()
+    assert np.array_equal(indptr, d["csr_indptr"])
+    assert np.array_equal(indices, d["csr_indices"])
+    cptr, cidx, perm = plan.pattern_csc()
+    assert np.array_equal(cptr, d["csc_indptr"])
+    assert np.array_equal(cidx, d["csc_indices"])
+    # perm maps CSC positions to CSR positions
+    rows = np.repeat(np.arange(plan.n_var), np.diff(indptr))
+    ccols = np.repeat(np.arange(plan.n_var), np.diff(cptr))
+    assert np.array_equal(rows[perm], cidx)
+    assert np.array_equal(indices[perm], ccols)
+
+
+def test_fused_eval_vs_reference_wf1(gfx):
+    d, s, plan = gfx
+    to_csr = csc_to_csr_perm(d["csc_indptr"], d["csc_indices"], d["csr_indptr"],
+                             d["csr_indices"])
+    for i, y in enumerate(d["ys"]):
+        g, j, norm = _eval(plan, y)
+        assert_parity(g, d["g_wf1"][i], f"g state {i}")
+        assert_parity(j, d["j_wf1"][i][to_csr], f"J state {i}")
+        assert norm == np.abs(g).max(initial=0.0)
+        assert_parity([norm], [np.abs(d["g_wf1"][i]).max(initial=0.0)], "norm")
+
+
+def test_residual_only_and_jacobian_only_modes(gfx):
+    d, s, plan = gfx
+    y = _dev(d["ys"][-1])
+    g_full, j_full, _ = _eval(plan, d["ys"][-1])
+    g = plan.empty(plan.n_var)
+    plan.eval(y, g=g)
+    j = plan.empty(plan.nnz)
+    plan.eval(y, jval=j)
+    torch.cuda.synchronize()
+    assert np.array_equal(g[: plan.n_var].cpu().numpy(), g_full)
+    assert np.array_equal(j[: plan.nnz].cpu().numpy(), j_full)
+
+
+def test_per_model_entry_points_vs_reference(gfx):
+    d, s, plan = gfx
+    y = _dev(d["ys"][-1])
+    li = [t.cpu().numpy() for t in plan.line_injections(y)]
+    for a, b in zip(li, d["line_inj"]):
+        assert_parity(a, b, "line injections")
+    slots = np.concatenate([plan.line_jacobian_slots(y).cpu().numpy().ravel(),
+                            plan.device_jacobian_slots(y).cpu().numpy()])
+    assert_parity(slots, d["slot_vals"], "slot values")
+    pool_dev = plan.device_injections(y).cpu().numpy()
+    assert_parity(pool_dev, d["dev_inj"], "device injections")
+    # generic join / assembly kernels on the reference's own index arrays
+    from paper_2011_11880_b200.plan import gather_sum, join_rows
+
+    i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device="cuda")
+    out = torch.empty(plan.n_var, dtype=torch.float64, device="cuda")
+    join_rows(i32(d["join_ptr"]), i32(d["join_split"]), i32(d["join_idx"]), _dev(d["pool"]), out)
+    assert np.array_equal(out.cpu().numpy(), d["g_wf1"][-1])
+    data = torch.empty(max(plan.nnz, 1), dtype=torch.float64, device="cuda")[: plan.nnz]
+    gather_sum(i32(d["gather_ptr"]), i32(d["slot_to_csc"]), _dev(d["slot_vals"]), data)
+    assert np.array_equal(data.cpu().numpy(), d["j_wf1"][-1])
+
+
+def test_host_dropin_workspaces(gfx):
+    d, s, plan = gfx
+    from paper_2011_11880_b200.jacobian import JacobianWorkspace, evaluate_jacobian
+    from paper_2011_11880_b200.residual import ResidualWorkspace, evaluate_residual
+
+    rws = ResidualWorkspace(s, plan)
+    jws = JacobianWorkspace(s, plan)
+    assert np.array_equal(jws.csc.indptr, d["csc_indptr"])
+    assert np.array_equal(jws.csc.indices, d["csc_indices"])
+    for i, y in enumerate(d["ys"]):
+        y = y.copy()
+        g = evaluate_residual(s, y, None, rws.residual, rws)
+        assert_parity(g, d["g_wf1"][i], "host g")
+        csc = evaluate_jacobian(s, y, None, jws)
+        assert csc is jws.csc
+        assert_parity(csc.data, d["j_wf1"][i], "host J")
+    with pytest.raises(ValueError):
+        rws.run(np.zeros(plan.n_var + 1), None)
+    with pytest.raises(ValueError):
+        evaluate_jacobian(build_system(synth.synth_case(3, 3, seed=0, pq_frac=0.5)), d["ys"][0],
+                          None, jws)
+
+
+def test_fd_agreement_small_cases():
+    """Analytic GPU Jacobian vs central differences of the GPU residual
+    (pflow/cli.py:161-176 check: worst relative error < 1e-6)."""
+    from paper_2011_11880_b200.jacobian import JacobianWorkspace, finite_difference_jacobian
+
+    for name in ("case14", "case5_shift", "tiny_edge"):
+        d = load(name)
+        s = system_of(d)
+        jws = JacobianWorkspace(s)
+        y = d["ys"][-1].copy()
+        jac = jws.run(y).toarray()
+        fd = finite_difference_jacobian(s, y)
+        err = np.abs(jac - fd) / np.maximum(1.0, np.abs(fd))
+        assert err.max() < 1e-6, name
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_synthetic_configs_vs_oracle(cfg):
+    s = build_system(synth.config_case(cfg, seed=cfg))
+    plan = _plan(s)
+    o = oracle.Oracle(s)
+    cptr, cidx = o.pattern_csc()
+    pptr, pidx, perm = plan.pattern_csc()
+    assert np.array_equal(cptr, pptr) and np.array_equal(cidx, pidx)
+    for k in range(2):
+        y = random_state(s, 100 * cfg + k)
+        g, j, norm = _eval(plan, y)
+        g_ref = o.residual(y)
+        j_ref = o.jacobian(y)
+        assert_parity(g, g_ref, f"cfg{cfg} g")
+        assert_parity(j[perm], j_ref, f"cfg{cfg} J")
+        assert norm == np.abs(g).max()
+
+
+def test_batched_golden_vs_reference():
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    d = load("batch_edge300")
+    s = system_of(d)
+    plan = _plan(s)
+    K = int(d["K"])
+    _, _, perm = plan.pattern_csc()
+    t = lambda a: _dev(to_blocked(a))
+    g = plan.empty(plan.n_var, K)
+    j = plan.empty(plan.nnz, K)
+    norms = plan.empty(K)
+    outage = torch.as_tensor(d["outage"].astype(np.int32), device="cuda")
+    plan.eval_batched(K, t(d["y"]), t(d["pq_p"]), t(d["pq_q"]), t(d["pv_p"]), outage, g, j, norms)
+    torch.cuda.synchronize()
+    G = from_blocked(g.cpu().numpy(), K, plan.n_var)
+    J = from_blocked(j.cpu().numpy(), K, plan.nnz)
+    for k in range(K):
+        assert_parity(G[k], d["g_wf1"][k], f"scenario {k} g")
+        assert_parity(J[k][perm], d["j_wf1"][k], f"scenario {k} J")
+    ref_norms = d["norms"]
+    assert np.all(np.abs(norms[:K].cpu().numpy() - ref_norms) <= 1e-14 + 1e-12 * ref_norms)
+    # CSC permutation kernel in batched layout
+    jc = plan.empty(plan.nnz, K)
+    plan.jac_to_csc(j, jc, K)
+    torch.cuda.synchronize()
+    JC = from_blocked(jc.cpu().numpy(), K, plan.nnz)
+    assert np.array_equal(JC, J[:, perm])
+
+
+def test_batched_config3_shape_vs_oracle():
+    """70k-bus config-3 topology, K = 64 scenarios (outages + load scaling);
+    every scenario checked against the oracle's mutated-system evaluation."""
+    from paper_2011_11880_b200.batched import ScenarioBuffers
+    from paper_2011_11880_b200.plan import to_blocked
+
+    s = build_system(synth.config_case(3, seed=3))
+    plan = _plan(s)
+    K = 64
+    sb = synth.make_scenarios(s, K, seed=7)
+    buf = ScenarioBuffers(plan, K)
+    buf.upload(sb)
+    buf.evaluate()
+    torch.cuda.synchronize()
+    o = oracle.Oracle(s)
+    _, _, perm = plan.pattern_csc()
+    G = buf.residual()
+    J = buf.jacobian_csr()
+    pick = [0, 1, 31, 32, 45, 63]
+    Kp = len(pick)
+    yk = sb.y[:, pick].T
+    g_ref, j_ref, n_ref = o.eval_scenarios(
+        Kp, to_blocked(yk), to_blocked(sb.pq_p[:, pick].T), to_blocked(sb.pq_q[:, pick].T),
+        to_blocked(sb.pv_p[:, pick].T), sb.outage[pick], nthreads=4)
+    from paper_2011_11880_b200.plan import from_blocked
+
+    g_ref = from_blocked(g_ref, Kp, plan.n_var)
+    j_ref = from_blocked(j_ref, Kp, plan.nnz)
+    for i, k in enumerate(pick):
+        assert_parity(G[k], g_ref[i], f"scenario {k} g")
+        assert_parity(J[k][perm], j_ref[i], f"scenario {k} J")
+    norms = buf.norms[:K].cpu().numpy()
+    assert np.array_equal(norms, np.abs(G).max(axis=1))
+
+
+def test_batched_k1_without_outage_equals_single():
+    s = build_system(synth.config_case(0, seed=0))
+    plan = _plan(s)
+    y = random_state(s, 5)
+    g1, j1, n1 = _eval(plan, y)
+    from paper_2011_11880_b200.plan import to_blocked
+
+    g = plan.empty(plan.n_var, 1)
+    j = plan.empty(plan.nnz, 1)
+    nrm = plan.empty(1)
+    plan.eval_batched(1, _dev(to_blocked(y[None, :])), g=g, jval=j, norms=nrm)
+    torch.cuda.synchronize()
+    assert np.array_equal(g.cpu().numpy().reshape(plan.n_var, 32)[:, 0], g1)
+    assert np.array_equal(j.cpu().numpy().reshape(plan.nnz, 32)[:, 0], j1)
+    assert float(nrm[0]) == n1
+
+
+def test_stress_hubs_config4_shape():
+    """Config-4 generator (hubs of degree ~50) at reduced size; all
+    scenarios vs oracle.  Full-size config 4 runs in the bench."""
+    from paper_2011_11880_b200.batched import ScenarioBuffers
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    s = build_system(synth.synth_case(20_000, 25_000, seed=9, pq_frac=0.6, pv_frac=0.15,
+                                      hub_frac=0.01, hub_degree=50, shunt_frac=0.05))
+    plan = _plan(s)
+    assert plan.max_degree >= 50
+    K = 40
+    sb = synth.make_scenarios(s, K, seed=2)
+    buf = ScenarioBuffers(plan, K)
+    buf.upload(sb)
+    buf.evaluate()
+    torch.cuda.synchronize()
+    o = oracle.Oracle(s)
+    _, _, perm = plan.pattern_csc()
+    g_ref, j_ref, n_ref = o.eval_scenarios(K, to_blocked(sb.y.T), to_blocked(sb.pq_p.T),
+                                           to_blocked(sb.pq_q.T), to_blocked(sb.pv_p.T),
+                                           sb.outage, nthreads=8)
+    G = buf.residual()
+    J = buf.jacobian_csr()
+    g_ref = from_blocked(g_ref, K, plan.n_var)
+    j_ref = from_blocked(j_ref, K, plan.nnz)
+    fails = sum(parity_failures(G[k], g_ref[k]) + parity_failures(J[k][perm], j_ref[k])
+                for k in range(K))
+    assert fails == 0
+
+
+def test_host_batched_pipeline_matches_device():
+    from paper_2011_11880_b200.batched import ScenarioBuffers
+    from paper_2011_11880_b200.plan import to_blocked
+
+    s = build_system(synth.config_case(0, seed=1))
+    plan = _plan(s)
+    K = 100
+    sb = synth.make_scenarios(s, K, seed=4)
+    buf = ScenarioBuffers(plan, K)
+    buf.upload(sb)
+    buf.evaluate()
+    torch.cuda.synchronize()
+    y = to_blocked(sb.y.T)
+    pq_p, pq_q, pv_p = to_blocked(sb.pq_p.T), to_blocked(sb.pq_q.T), to_blocked(sb.pv_p.T)
+    g = np.zeros_like(y)
+    j = np.zeros(buf.jval.numel())
+    norms = np.zeros(K)
+    plan.eval_batched_host(K, y, pq_p, pq_q, pv_p, sb.outage.astype(np.int32), g, j, norms,
+                           blocks_per_stage=1, n_streams=3)
+    assert np.array_equal(g, buf.g.cpu().numpy()[: g.size])
+    assert np.array_equal(j, buf.jval.cpu().numpy()[: j.size])
+    assert np.array_equal(norms, buf.norms[:K].cpu().numpy())
+
+
+def test_errors_are_loud():
+    s = build_system(synth.config_case(0, seed=0))
+    plan = _plan(s)
+    with pytest.raises(ValueError):
+        plan.eval(torch.zeros(3, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        plan.eval(torch.zeros(plan.n_var, dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        plan.eval_host(np.zeros(plan.n_var - 1))
+
+
+def test_deterministic_repeat():
+    s = build_system(synth.config_case(1, seed=1))
+    plan = _plan(s)
+    y = random_state(s, 1)
+    a = _eval(plan, y)
+    b = _eval(plan, y)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    plan2 = _plan(s)
+    assert all(np.array_equal(x, y_) for x, y_ in zip(plan.pattern_csr(), plan2.pattern_csr()))
