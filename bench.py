@@ -1,0 +1,389 @@
+"""Benchmark: f+J evaluations/s on the 70k-bus synthetic grid (BASELINE.json).
+
+Workload (per rank, weak scaling): BASELINE config 3 - the config-2-shaped
+70,000-bus / 88,000-branch grid shared by K = 256 scenarios (per-device load
+scaling U(0.8,1.2), PV scaling U(0.5,1.5), one outaged branch each).  One
+step = one fused residual + Jacobian + infinity-norm evaluation of all K
+scenarios on the GPU (``pf_eval_batched``), followed on N > 1 by the NCCL
+all-gather of the per-scenario norms.  Inputs are resident in HBM; the step
+moves ~2.8 GB, more than the 126 MB L2, so no flush is needed.
+
+Extra lines of evidence in the same JSON object:
+  roofline      algorithmic bytes / measured kernel time vs MEASURED_PEAKS.json
+  e2e           the same metric through the host-buffer C ABI
+                (pf_eval_batched_host: H2D inputs, D2H g + J + norms)
+  cpu_baseline  the CPU oracle port (C restatement of pflow) on this host
+  single_grid   config 2 single grid (one 70k evaluation, L2 flushed between)
+
+``--impl reference`` times the reference algorithm's CPU restatement (the
+oracle port; pflow itself is Python and does not travel to the GPU box) with
+all host threads on the same workload and prints the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "f+J evals/s on 70k-bus synthetic grid (fp64); HBM GB/s as % of peak"
+K_PER_RANK = 256
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(sys_, nnz: int, K: int) -> tuple[int, int, int]:
+    """per-scenario bytes and shared static bytes per launch."""
+    n_var = sys_.n_var
+    P, G, S, L = len(sys_.pq), len(sys_.pv), len(sys_.slack), len(sys_.lines)
+    per_scen = 8 * n_var + 16 * P + 8 * G + 4 + 8 * n_var + 8 * nnz + 8
+    coef = 8 * (8 if sys_.lines.has_shift else 6)
+    static = L * (8 + coef) + 4 * P + 12 * G + 20 * S
+    return per_scen, static, per_scen * K + static
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.2)
+        self.p.terminate()
+        self.p.wait()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 8 and r[1].strip().isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 8 and r[2].strip().isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 8 for i in range(4)
+                          if r[4 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def build_case(seed: int = 3):
+    from paper_2011_11880_b200 import synth
+    from paper_2011_11880_b200.system_model import build_system
+
+    return build_system(synth.config_case(3, seed=seed))
+
+
+def blocked_inputs(sys_, K, seed):
+    from paper_2011_11880_b200 import synth
+    from paper_2011_11880_b200.plan import to_blocked
+
+    sb = synth.make_scenarios(sys_, K, seed)
+    return (to_blocked(sb.y.T), to_blocked(sb.pq_p.T), to_blocked(sb.pq_q.T),
+            to_blocked(sb.pv_p.T), sb.outage.astype(np.int32))
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle port on host cores
+# ---------------------------------------------------------------------------
+
+def cpu_reference(sys_, K, seed, steps, warmup, threads, min_seconds=0.0):
+    """Time the C restatement of pflow over K scenarios per step.
+
+    Each scenario: mutate loads / PV P / outage coefficients, run the
+    reference's residual (pool + join) and Jacobian (slots + CSC gather)
+    algorithm, restore.  Outputs stay in
+    each thread's workspace as in pflow (the workspace owns the CSC).
+    """
+    import oracle  # reference arm / cpu_baseline only
+
+    o = oracle.Oracle(sys_)
+    y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K, seed)
+    best = None
+    for wf in (5, 1):  # pflow's fastest CPU workflows at 70k
+        t0 = time.perf_counter()
+        o.eval_scenarios(K, y, pq_p, pq_q, pv_p, outage, want_g=False, want_j=False, wf=wf,
+                         nthreads=threads)
+        dt = time.perf_counter() - t0
+        if best is None or dt < best[1]:
+            best = (wf, dt)
+    wf = best[0]
+    for _ in range(max(0, warmup - 1)):
+        o.eval_scenarios(K, y, pq_p, pq_q, pv_p, outage, want_g=False, want_j=False, wf=wf,
+                         nthreads=threads)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < steps or (time.perf_counter() - t_start) < min_seconds:
+        t0 = time.perf_counter()
+        o.eval_scenarios(K, y, pq_p, pq_q, pv_p, outage, want_g=False, want_j=False, wf=wf,
+                         nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    return {"value": K * len(times) / total, "ms_per_step": 1e3 * total / len(times),
+            "wf": wf, "steps": len(times), "threads": threads}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys_ = build_case()
+    threads = os.cpu_count() or 1
+    r = cpu_reference(sys_, K_PER_RANK, 1000, args.steps, args.warmup, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config3: 70k-bus/88k-branch grid, K=256 scenarios per step "
+                               "(load/PV scaling + 1 outage each), f+J per scenario",
+                   "parallelism": f"{threads} host threads, one scenario per thread at a time"},
+        "cpu_baseline": {"value": r["value"], "unit": "evals/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{r['steps']} steps x {K_PER_RANK} scenarios, pflow wf{r['wf']} "
+                                   "restated in C (oracle/), workspace outputs"},
+        "e2e": {"value": r["value"], "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2011_11880_b200.plan import Plan, launch_count
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    K = K_PER_RANK
+    sys_ = build_case()
+    plan = Plan(sys_, device=dev)
+    per_scen, static, bytes_launch = algorithmic_bytes(sys_, plan.nnz, K)
+    y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K, seed=1000 + rank)
+    t = lambda a, dt=torch.float64: torch.from_numpy(a).to(dev, dt)
+    d_y, d_pqp, d_pqq, d_pvp = t(y), t(pq_p), t(pq_q), t(pv_p)
+    d_out = torch.from_numpy(outage).to(dev)
+    d_g = plan.empty(plan.n_var, K)
+    d_j = plan.empty(plan.nnz, K)
+    d_n = plan.empty(K)
+    stream = torch.cuda.current_stream(dev)
+    gathered = torch.empty(world * K, dtype=torch.float64, device=dev)
+
+    def step():
+        plan.eval_batched(K, d_y, d_pqp, d_pqq, d_pvp, d_out, d_g, d_j, d_n, stream=stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, d_n)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    clocks = Clocks(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = launch_count()
+    start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        plan.eval_batched(K, d_y, d_pqp, d_pqq, d_pvp, d_out, d_g, d_j, d_n, stream=stream)
+        ev[i][1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, d_n)
+    end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = launch_count() - l0
+    clk = clocks.stop()
+    ms_total = start.elapsed_time(end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    ms_t = torch.tensor([ms_total, statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_total, kern_avg = float(ms_t[0]), float(ms_t[1])
+    value = world * K * args.steps / (ms_total / 1e3)
+    peak, peak_kind = peaks()
+    achieved = bytes_launch / (kern_avg / 1e3) / 1e9
+
+    # norms sanity (device-resident result used by Newton callers)
+    assert torch.isfinite(d_n[:K]).all()
+
+    # ---- e2e through the host-buffer C ABI (pinned host memory) ----
+    del d_y, d_pqp, d_pqq, d_pvp, d_out
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+    h_y, h_pqp, h_pqq, h_pvp, h_out = pin(y), pin(pq_p), pin(pq_q), pin(pv_p), pin(outage)
+    h_g = torch.empty(d_g.numel(), dtype=torch.float64).pin_memory().numpy()
+    h_j = torch.empty(d_j.numel(), dtype=torch.float64).pin_memory().numpy()
+    h_n = torch.empty(K, dtype=torch.float64).pin_memory().numpy()
+    bi = h_y.nbytes + h_pqp.nbytes + h_pqq.nbytes + h_pvp.nbytes + h_out.nbytes
+    bo = h_g.nbytes + h_j.nbytes + h_n.nbytes
+    e2e_steps = max(2, min(args.steps, 5))
+
+    def host_step():
+        plan.eval_batched_host(K, h_y, h_pqp, h_pqq, h_pvp, h_out, h_g, h_j, h_n,
+                               blocks_per_stage=1, n_streams=4)
+
+    host_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        host_step()
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * K * e2e_steps / float(e2e_s[0])
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {
+                "workload": "config3: 70k-bus/88k-branch grid (45k PQ, 6k PV, 1 slack), "
+                            f"K={K} scenarios per GPU per step, per-device load U(0.8,1.2) + "
+                            "PV U(0.5,1.5) scaling, 1 outaged branch each; fused f+J+inf-norm",
+                "n_var": plan.n_var, "nnz": plan.nnz, "scenarios_per_gpu": K,
+                "parallelism": f"scenario-sharded x{world}" + (", NCCL all-gather of norms"
+                                                               if world > 1 else ""),
+                "l2": "inputs+outputs per step 2.8 GB > 126 MB L2 (no flush needed)",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": bytes_launch,
+                         "bytes_per_scenario": per_scen, "static_bytes": static,
+                         "kernel_ms": kern_avg, "kernel": "k_eval_batched<RES|JAC|NORM>"},
+            "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": bi,
+                    "d2h_bytes_per_step": bo, "api": "pf_eval_batched_host (pinned host buffers)",
+                    "steps": e2e_steps},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+    if world > 1:
+        dist.barrier()
+
+    if rank == 0 and world == 1 and not args.no_single:
+        line["single_grid"] = single_grid(plan_cache=None, dev=dev, steps=max(20, args.steps))
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        r = cpu_reference(sys_, K, 2000, 1, 1, threads, min_seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": r["value"], "unit": "evals/s", "cores": threads, "kind": "port",
+            "sample": f"{r['steps']} x {K} config-3 scenarios, pflow wf{r['wf']} restated in C "
+                      "(oracle/), one scenario per thread, workspace outputs"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def single_grid(plan_cache, dev, steps: int) -> dict:
+    """Config 2: one 70k-bus grid, f+J+norm per evaluation, L2 flushed between."""
+    import torch
+
+    from paper_2011_11880_b200 import synth
+    from paper_2011_11880_b200.plan import Plan
+    from paper_2011_11880_b200.system_model import build_system, random_state
+
+    s = build_system(synth.config_case(2, seed=2))
+    plan = Plan(s, device=dev)
+    per_scen, static, bytes_launch = algorithmic_bytes(s, plan.nnz, 1)
+    # single grid: loads come from the plan (PQ p0/q0 read from device params)
+    bytes_launch = (8 * s.n_var + 8 * s.n_var + 8 * plan.nnz + 8 + static
+                    + 16 * len(s.pq) + 8 * len(s.pv))
+    y = torch.as_tensor(random_state(s, 7), device=dev)
+    g, j, n = plan.empty(plan.n_var), plan.empty(plan.nnz), plan.empty(1)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    for _ in range(5):
+        plan.eval(y, g, j, n, stream=st)
+    times = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        plan.eval(y, g, j, n, stream=st)
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        times.append(a.elapsed_time(b))
+    med = statistics.median(times)
+    peak, _ = peaks()
+    gbs = bytes_launch / (med / 1e3) / 1e9
+    return {"workload": "config2: 70k buses, 88k branches, one f+J+norm (cold L2)",
+            "evals_per_s": 1e3 / med, "us_per_eval": med * 1e3, "us_min": min(times) * 1e3,
+            "algorithmic_bytes": bytes_launch, "achieved_gbs": gbs, "frac": gbs / peak,
+            "n_var": plan.n_var, "nnz": plan.nnz}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-single", action="store_true", help="skip the single-grid leg")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -167,6 +167,10 @@ PF_API int pf_join_rows(int32_t n_rows, const int32_t* ptr, const int32_t* split
 PF_API int pf_gather_sum(int32_t n_rows, const int32_t* ptr, const int32_t* idx, const double* vals,
                   double* out, void* stream);
 
+/* sin/cos over an array with the engine's trig routine (device pointers);
+ * test surface like pflow kernels.py:66-72 `sincos`. */
+PF_API int pf_sincos(int64_t n, const double* x, double* s, double* c, void* stream);
+
 /* Number of kernels this library has launched (process-wide counter). */
 PF_API int64_t pf_launch_count(void);
 

@@ -55,6 +55,7 @@ def lib():
             "orc_ws_vals": (_VP, [_VP]),
             "orc_line_injections": (None, [_VP, C.c_int, _VP, _VP, _VP, _VP, _VP]),
             "orc_sincos_poly": (None, [_VP, _VP, _VP, C.c_int64]),
+            "orc_libm_sincos": (None, [_VP, _VP, _VP, C.c_int64]),
             "orc_eval_threaded": (None, [_VP, _VP, _VP, _VP, C.c_int]),
             "orc_eval_scenarios": (C.c_int, [_VP, C.c_int, C.c_int32, _VP, _VP, _VP, _VP, _VP,
                                              _VP, _VP, _VP, C.c_int]),
@@ -171,4 +172,12 @@ def sincos_poly(x):
     x = np.ascontiguousarray(x, dtype=np.float64)
     s, c = np.zeros_like(x), np.zeros_like(x)
     lib().orc_sincos_poly(_p(x), _p(s), _p(c), x.size)
+    return s, c
+
+
+def libm_sincos(x):
+    """glibc sin/cos (what pflow wf1 calls through @llvm.sin/cos.f64)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s, c = np.zeros_like(x), np.zeros_like(x)
+    lib().orc_libm_sincos(_p(x), _p(s), _p(c), x.size)
     return s, c

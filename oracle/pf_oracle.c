@@ -560,6 +560,13 @@ void orc_eval_threaded(orc_ws* w, const double* y, double* g, double* csc_data, 
     }
 }
 
+void orc_libm_sincos(const double* x, double* s, double* c, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) {
+        s[i] = sin(x[i]);
+        c[i] = cos(x[i]);
+    }
+}
+
 /* ------------------------------------------------------------------ */
 /* scenario batch (SURVEY.md §8c batched oracle)                        */
 /* ------------------------------------------------------------------ */

@@ -53,6 +53,7 @@ const double* orc_ws_pool(const orc_ws* w);
 const double* orc_ws_vals(const orc_ws* w);
 void orc_line_injections(orc_ws* w, int wf, const double* y, double* ph, double* pk,
                          double* qh, double* qk);
+void orc_libm_sincos(const double* x, double* s, double* c, int64_t n);
 void orc_sincos_poly(const double* x, double* s, double* c, int64_t n);
 
 /* wf3: intra-model chunks over nthreads (OpenMP); residual + CSC Jacobian */

@@ -100,6 +100,7 @@ _SIGS = {
     "pf_device_jacobian_slots": (C.c_int, [_VP, _VP, _VP, _VP]),
     "pf_join_rows": (C.c_int, [C.c_int32, _VP, _VP, _VP, _VP, _VP, _VP]),
     "pf_gather_sum": (C.c_int, [C.c_int32, _VP, _VP, _VP, _VP, _VP]),
+    "pf_sincos": (C.c_int, [C.c_int64, _VP, _VP, _VP, _VP]),
     "pf_launch_count": (C.c_int64, []),
 }
 

@@ -3,7 +3,9 @@
 // Compiled with -fmad=false: every product and sum is rounded exactly where
 // the reference's wf1 rounds it (numba njit without fastmath, pflow
 // kernels.py:79-282), so the only deviation from the CPU oracle is the last
-// ulp of CUDA's sincos versus glibc's sin/cos.
+// rounding of sin/cos: pf_trig.h is correctly rounded except in rare
+// near-midpoint cases, and glibc 2.39 is not correctly rounded in ~0.3% of
+// power-flow angles, so the two agree on >99.7% of arguments.
 //
 // Fused kernel k_eval (the product path): one thread per (bus, scenario).
 // A bus walks its incidence list -- branches with h = bus ascending, then
@@ -20,11 +22,25 @@
 #include <cuda_runtime.h>
 
 #include "pf_internal.cuh"
+#include "pf_trig.h"
 
 namespace pf {
 namespace {
 
 constexpr int RES = 1, JAC = 2, NORM = 4;
+
+// The one trig routine every kernel uses (fused, per-model, test surface):
+// near-correctly-rounded table sin/cos (pf_trig.h), table staged in shared
+// memory because lanes index it divergently.
+__device__ __forceinline__ void pf_sincos(double x, const double* tab, double* s, double* c) {
+    pf_sincos_tab(x, tab, s, c);
+}
+
+__device__ __forceinline__ const double* stage_trig_table(double* smem) {
+    for (int t = threadIdx.x; t < PF_TRIG_N * 4; t += blockDim.x) smem[t] = pf_trig_tab[t];
+    __syncthreads();
+    return smem;
+}
 
 __device__ __forceinline__ double4 ldg4(const double4* p) {
     const double2* q = reinterpret_cast<const double2*>(p);
@@ -56,7 +72,8 @@ __device__ __forceinline__ void put_offdiag(double* __restrict__ jv, int64_t at,
 
 template <int MODE, bool BATCH>
 __device__ __forceinline__ unsigned long long eval_bus(
-    const DevicePlan& d, const int32_t i, const Addr<BATCH>& A, const int32_t out_l,
+    const DevicePlan& d, const double* tab, const int32_t i, const Addr<BATCH>& A,
+    const int32_t out_l,
     const double* __restrict__ y, const double* __restrict__ pq_p,
     const double* __restrict__ pq_q, const double* __restrict__ pv_p,
     double* __restrict__ g, double* __restrict__ jv) {
@@ -85,7 +102,7 @@ __device__ __forceinline__ unsigned long long eval_bus(
         // thk = theta_h - theta_k (kernels.py:86)
         const double thk = kside ? (th_j - th_i) : (th_i - th_j);
         double si, ci;
-        sincos(thk, &si, &ci);
+        pf_sincos(thk, tab, &si, &ci);
         const double ab = u * w;
         // h side: t1h = gl ci + bl si, t2h = gl si - bl ci.  k side with
         // b1 = -bl2: t1k = gl2 ci - bl2 si, and t2s = -t2k.  Sign flips are
@@ -197,6 +214,8 @@ __global__ void __launch_bounds__(32 * W) k_eval_batched(
     const double* __restrict__ pv_p, const int32_t* __restrict__ outage,
     double* __restrict__ g, double* __restrict__ jv, unsigned long long* __restrict__ norms) {
     __shared__ unsigned long long red[W][32];
+    __shared__ double s_tab[PF_TRIG_N * 4];
+    const double* tab = stage_trig_table(s_tab);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t bus = blockIdx.x * W + warp;
     const int64_t blk = blockIdx.y;
@@ -209,7 +228,7 @@ __global__ void __launch_bounds__(32 * W) k_eval_batched(
         A.pq0 = blk * (int64_t)d.P * PF_LANES + lane;
         A.pv0 = blk * (int64_t)d.G * PF_LANES + lane;
         const int32_t out_l = outage ? __ldg(outage + s) : -1;
-        nrm = eval_bus<MODE, true>(d, bus, A, out_l, y, pq_p, pq_q, pv_p, g, jv);
+        nrm = eval_bus<MODE, true>(d, tab, bus, A, out_l, y, pq_p, pq_q, pv_p, g, jv);
     }
     if (MODE & NORM) {
         red[warp][lane] = nrm;
@@ -230,11 +249,13 @@ __global__ void __launch_bounds__(128) k_eval_single(const DevicePlan d,
                                                      double* __restrict__ jv,
                                                      unsigned long long* __restrict__ norm) {
     __shared__ unsigned long long red[4];
+    __shared__ double s_tab[PF_TRIG_N * 4];
+    const double* tab = stage_trig_table(s_tab);
     const int32_t bus = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long nrm = 0;
     if (bus < d.N) {
         Addr<false> A{0, 0, 0, 0};
-        nrm = eval_bus<MODE, false>(d, bus, A, -1, y, nullptr, nullptr, nullptr, g, jv);
+        nrm = eval_bus<MODE, false>(d, tab, bus, A, -1, y, nullptr, nullptr, nullptr, g, jv);
     }
     if (MODE & NORM) {
         for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
@@ -252,6 +273,8 @@ __global__ void __launch_bounds__(128) k_eval_single(const DevicePlan d,
 // kernels.py:79-97, same expressions
 __global__ void k_line_injections(const DevicePlan d, const double* __restrict__ y,
                                   double* ph, double* pk, double* qh, double* qk) {
+    __shared__ double s_tab[PF_TRIG_N * 4];
+    const double* tab = stage_trig_table(s_tab);
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.L) return;
     const int32_t h = d.bus_h[i], k = d.bus_k[i], nb = d.N;
@@ -259,7 +282,7 @@ __global__ void k_line_injections(const DevicePlan d, const double* __restrict__
     const double b = y[nb + k];
     const double thk = y[h] - y[k];
     double si, ci;
-    sincos(thk, &si, &ci);
+    pf_sincos(thk, tab, &si, &ci);
     const double ab = a * b;
     const double t1h = d.gl[i] * ci + d.bl[i] * si;
     const double t2h = d.gl[i] * si - d.bl[i] * ci;
@@ -273,6 +296,8 @@ __global__ void k_line_injections(const DevicePlan d, const double* __restrict__
 
 // kernels.py:128-163; o = [16][L] in jacobian.py:31-36 order
 __global__ void k_line_jac_slots(const DevicePlan d, const double* __restrict__ y, double* o) {
+    __shared__ double s_tab[PF_TRIG_N * 4];
+    const double* tab = stage_trig_table(s_tab);
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.L) return;
     const int64_t L = d.L;
@@ -281,7 +306,7 @@ __global__ void k_line_jac_slots(const DevicePlan d, const double* __restrict__ 
     const double b = y[nb + k];
     const double thk = y[h] - y[k];
     double si, ci;
-    sincos(thk, &si, &ci);
+    pf_sincos(thk, tab, &si, &ci);
     const double ab = a * b;
     const double t1h = d.gl[i] * ci + d.bl[i] * si;
     const double t2h = d.gl[i] * si - d.bl[i] * ci;
@@ -412,6 +437,15 @@ __global__ void k_jac_to_csc(int32_t nnz, int32_t nblk, const int32_t* __restric
     if (q >= nnz) return;
     const int64_t base = blk * (int64_t)nnz * PF_LANES + lane;
     dst[base + q * PF_LANES] = src[base + (int64_t)__ldg(perm + q) * PF_LANES];
+}
+
+// array sin/cos test surface (pflow kernels.py:66-72 exposes the same)
+__global__ void k_sincos(int64_t n, const double* __restrict__ x, double* __restrict__ s,
+                         double* __restrict__ c) {
+    __shared__ double s_tab[PF_TRIG_N * 4];
+    const double* tab = stage_trig_table(s_tab);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) pf_sincos(x[i], tab, s + i, c + i);
 }
 
 inline unsigned grid_for(int64_t n, int threads) {
@@ -550,6 +584,13 @@ cudaError_t launch_gather_sum(int32_t n, const int32_t* ptr, const int32_t* idx,
                               const double* vals, double* out, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     k_gather_sum<<<grid_for(n, 256), 256, 0, st>>>(n, ptr, idx, vals, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sincos(int64_t n, const double* x, double* s, double* c, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_sincos<<<grid_for(n, 256), 256, 0, st>>>(n, x, s, c);
     count_launch();
     return cudaGetLastError();
 }

@@ -110,6 +110,7 @@ cudaError_t launch_device_jac_slots(const DevicePlan& d, const double* y, double
 cudaError_t launch_join_rows(int32_t n, const int32_t* ptr, const int32_t* split,
                              const int32_t* idx, const double* pool, double* out,
                              cudaStream_t st);
+cudaError_t launch_sincos(int64_t n, const double* x, double* s, double* c, cudaStream_t st);
 cudaError_t launch_gather_sum(int32_t n, const int32_t* ptr, const int32_t* idx,
                               const double* vals, double* out, cudaStream_t st);
 

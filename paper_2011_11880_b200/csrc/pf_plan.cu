@@ -185,7 +185,7 @@ __global__ void k_row_len(int32_t N, int32_t n_gen, int32_t S, const int32_t* ub
         int32_t nv = nb > 0 ? nb : (sh ? 1 : 0);
         rowlen[i] = nb + nv + n_sl;
         rowlen[N + i] = nb + nv + n_pv + n_sl;
-    } else if (t < 2 * (int64_t)N + n_gen + S) {
+    } else if (t >= 2 * (int64_t)N && t < 2 * (int64_t)N + n_gen + S) {
         rowlen[t] = 1;
     }
 }
@@ -837,6 +837,13 @@ int pf_gather_sum(int32_t n, const int32_t* ptr, const int32_t* idx, const doubl
     if (n < 0) return pf::invalid("n < 0");
     if (n > 0 && (!ptr || !out)) return pf::invalid("NULL argument");
     PF_CUDA(pf::launch_gather_sum(n, ptr, idx, vals, out, (cudaStream_t)stream));
+    return PF_OK;
+}
+
+int pf_sincos(int64_t n, const double* x, double* s, double* c, void* stream) {
+    if (n < 0) return pf::invalid("n < 0");
+    if (n > 0 && (!x || !s || !c)) return pf::invalid("NULL argument");
+    PF_CUDA(pf::launch_sincos(n, x, s, c, (cudaStream_t)stream));
     return PF_OK;
 }
 

@@ -224,6 +224,16 @@ def gather_sum(ptr_, idx, vals, out, stream=None) -> None:
                               out.data_ptr(), _stream_ptr(stream)))
 
 
+def sincos(x, stream=None):
+    """(sin x, cos x) with the engine's device trig (CUDA float64 tensor in)."""
+    torch = _torch()
+    x = x.contiguous()
+    s, c = torch.empty_like(x), torch.empty_like(x)
+    check(lib().pf_sincos(x.numel(), x.data_ptr(), s.data_ptr(), c.data_ptr(),
+                          _stream_ptr(stream)))
+    return s, c
+
+
 def launch_count() -> int:
     """Kernels libpfgpu has launched in this process."""
     return int(lib().pf_launch_count())

@@ -296,8 +296,10 @@ def test_host_batched_pipeline_matches_device():
     norms = np.zeros(K)
     plan.eval_batched_host(K, y, pq_p, pq_q, pv_p, sb.outage.astype(np.int32), g, j, norms,
                            blocks_per_stage=1, n_streams=3)
-    assert np.array_equal(g, buf.g.cpu().numpy()[: g.size])
-    assert np.array_equal(j, buf.jval.cpu().numpy()[: j.size])
+    from paper_2011_11880_b200.plan import from_blocked
+
+    assert np.array_equal(from_blocked(g, K, plan.n_var), buf.residual())
+    assert np.array_equal(from_blocked(j, K, plan.nnz), buf.jacobian_csr())
     assert np.array_equal(norms, buf.norms[:K].cpu().numpy())
 
 
@@ -321,3 +323,18 @@ def test_deterministic_repeat():
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     plan2 = _plan(s)
     assert all(np.array_equal(x, y_) for x, y_ in zip(plan.pattern_csr(), plan2.pattern_csr()))
+
+
+def test_gpu_trig_bit_identical_to_cpu_twin(tmp_path):
+    from test_trig import build_twin, sample, twin_sincos
+
+    from paper_2011_11880_b200.plan import sincos
+
+    x = sample(200000, seed=5)
+    s_ref, c_ref = twin_sincos(build_twin(tmp_path), x)
+    s, c = sincos(torch.as_tensor(x, device="cuda"))
+    s, c = s.cpu().numpy(), c.cpu().numpy()
+    finite = np.abs(x) < 2.0 ** 20
+    assert np.array_equal(s[finite], s_ref[finite])
+    assert np.array_equal(c[finite], c_ref[finite])
+    assert np.array_equal(np.signbit(s[finite]), np.signbit(s_ref[finite]))
