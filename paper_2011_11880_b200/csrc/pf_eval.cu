@@ -21,13 +21,16 @@
 // store is one fully coalesced 256-byte transaction (PF_LANES-blocked layout).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "pf_internal.cuh"
 #include "pf_trig.h"
 
 namespace pf {
 namespace {
 
-constexpr int RES = 1, JAC = 2, NORM = 4;
+constexpr int RES = 1, JAC = 2, NORM = 4, CHEAP_TRIG = 8;  // CHEAP_TRIG: dev experiment only
 
 // The one trig routine every kernel uses (fused, per-model, test surface):
 // near-correctly-rounded table sin/cos (pf_trig.h), table staged in shared
@@ -53,127 +56,158 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
     return static_cast<unsigned long long>(__double_as_longlong(fabs(x)));
 }
 
-template <bool BATCH>
-struct Addr {
-    int64_t y0, j0, pq0, pv0;  // element offset of entry 0 of this scenario
-    __device__ __forceinline__ int64_t y(int64_t e) const { return BATCH ? y0 + e * PF_LANES : e; }
-    __device__ __forceinline__ int64_t j(int64_t e) const { return BATCH ? j0 + e * PF_LANES : e; }
-    __device__ __forceinline__ int64_t pq(int64_t e) const { return pq0 + e * PF_LANES; }
-    __device__ __forceinline__ int64_t pv(int64_t e) const { return pv0 + e * PF_LANES; }
+// Per-thread view of one scenario: base pointers already offset to the
+// thread's scenario block and lane, so entry e sits at base[e * S] with
+// S = PF_LANES (batched) or 1 (single grid).  Offsets stay 32-bit
+// (pf_plan_create checks nnz * PF_LANES < 2^31).
+template <int S>
+struct Scen {
+    const double* __restrict__ y;
+    const double* __restrict__ pq_p;
+    const double* __restrict__ pq_q;
+    const double* __restrict__ pv_p;
+    double* __restrict__ g;
+    double* __restrict__ j;
+    int32_t out_l;
 };
 
-template <int MODE>
-__device__ __forceinline__ void put_offdiag(double* __restrict__ jv, int64_t at, bool first,
+// Outputs are written once and never re-read by the kernel (except the rare
+// parallel-branch update), so store them evict-first: the 2.3 GB/step output
+// stream must not push the scenario states out of L2.
+__device__ __forceinline__ void st_out(double* p, double v) { __stcs(p, v); }
+
+template <int S>
+__device__ __forceinline__ void put_offdiag(double* __restrict__ jv, int32_t at, bool first,
                                             double v) {
     // reference assembly: acc = 0.0; acc += slot ... (kernels.py:277-282)
-    if (first) jv[at] = 0.0 + v;
-    else jv[at] = jv[at] + v;
+    if (first) st_out(jv + at * S, 0.0 + v);
+    else st_out(jv + at * S, jv[at * S] + v);
 }
 
-template <int MODE, bool BATCH>
-__device__ __forceinline__ unsigned long long eval_bus(
-    const DevicePlan& d, const double* tab, const int32_t i, const Addr<BATCH>& A,
-    const int32_t out_l,
-    const double* __restrict__ y, const double* __restrict__ pq_p,
-    const double* __restrict__ pq_q, const double* __restrict__ pv_p,
-    double* __restrict__ g, double* __restrict__ jv) {
+// One incidence of bus i (kernels.py:79-163 restated for one terminal):
+// adds the flow to the bus balance, the partials to the four diagonal
+// accumulators, and writes the four off-diagonal values of this neighbour.
+template <int MODE, int S>
+__device__ __forceinline__ void incidence(const double* tab, const int4 m, double4 c,
+                                          const double th_i, const double u, const double th_j,
+                                          const double w, const int32_t out_l,
+                                          double* __restrict__ jv, const int32_t rp,
+                                          const int32_t rq, const int32_t nb, double& acc_p,
+                                          double& acc_q, double& d_pt, double& d_pv,
+                                          double& d_qt, double& d_qv) {
+    constexpr bool BATCH = S > 1;
+    if (BATCH && m.y == out_l) c = make_double4(0.0, 0.0, 0.0, 0.0);  // outage
+    const bool kside = (m.z & KSIDE) != 0;
+    // thk = theta_h - theta_k (kernels.py:86)
+    const double thk = kside ? (th_j - th_i) : (th_i - th_j);
+    double si, ci;
+    if (MODE & CHEAP_TRIG) {
+        si = thk;
+        ci = 1.0 - thk;
+    } else {
+        pf_sincos(thk, tab, &si, &ci);
+    }
+    const double ab = u * w;
+    // h side: t1h = gl ci + bl si, t2h = gl si - bl ci.  k side with
+    // b1 = -bl2: t1k = gl2 ci - bl2 si, and t2s = -t2k.  Sign flips are
+    // exact, so every term is bit-identical to kernels.py:90-163.
+    const double t1 = c.x * ci + c.y * si;
+    const double t2 = c.x * si - c.y * ci;
+    const double t2s = kside ? -t2 : t2;
+    const double uu = u * u;                     // (-u)*u == -(u*u) exactly
+    acc_p -= uu * c.z - ab * t1;                 // ph / pk
+    acc_q -= -(uu * c.w) - ab * t2s;             // qh / qk
+    if (MODE & JAC) {
+        d_pt += -ab * t2s;                       // gph_thh | gpk_thk
+        d_pv += -(2.0 * u * c.z - w * t1);       // gph_vh  | gpk_vk
+        d_qt += ab * t1;                         // gqh_thh | gqk_thk
+        d_qv += 2.0 * u * c.w + w * t2s;         // gqh_vh  | gqk_vk
+        const bool first = (m.z & FIRST) != 0;
+        const int32_t pos = m.z & POS_MASK;
+        put_offdiag<S>(jv, rp + pos, first, ab * t2s);        // gph_thk | gpk_thh
+        put_offdiag<S>(jv, rp + nb + pos, first, u * t1);     // gph_vk  | gpk_vh
+        put_offdiag<S>(jv, rq + pos, first, -ab * t1);        // gqh_thk | gqk_thh
+        put_offdiag<S>(jv, rq + nb + pos, first, u * t2s);    // gqh_vk  | gqk_vh
+    }
+}
+
+// One bus for one scenario (S = PF_LANES: batched lane; S = 1: single grid).
+// U incidences are fetched together (metadata + neighbour states) before
+// their arithmetic runs in list order, so U gathers are in flight at once.
+template <int MODE, int S, int U>
+__device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, const double* tab,
+                                                       const int32_t i, const Scen<S>& A,
+                                                       const int32_t ln, const int32_t out_l) {
+    constexpr bool BATCH = S > 1;
     const int32_t N = d.N;
-    const double th_i = y[A.y(i)];
-    const double v_i = y[A.y(N + i)];
-    const int4 br = __ldg(d.bus_row + i);
-    const int64_t rp = br.x, rq = br.y, nb = br.z;
+    const double* __restrict__ y = A.y + ln;
+    double* __restrict__ jv = A.j ? A.j + ln : nullptr;
+    const int4 br = __ldg(d.bus_row + 2 * i);
+    const int4 rng = __ldg(d.bus_row + 2 * i + 1);
+    const int32_t rp = br.x, rq = br.y, nb = br.z;
     const int32_t pos_i = br.w & POS_MASK;
     const bool vdiag = (br.w & VDIAG) != 0;
+    const int32_t e0 = rng.x, e1 = rng.y;
+    const double th_i = y[i * S];
+    const double v_i = y[(N + i) * S];
 
     double acc_p = 0.0, acc_q = 0.0;
     double d_pt = 0.0, d_pv = 0.0, d_qt = 0.0, d_qv = 0.0;
     unsigned long long nrm = 0;
 
-    const int32_t e1 = __ldg(d.inc_ptr + i + 1);
-    for (int32_t e = __ldg(d.inc_ptr + i); e < e1; ++e) {
+    for (int32_t e = e0; e < e1; ++e) {
         const int4 m = __ldg(d.inc_meta + e);
-        double4 c = ldg4(d.inc_coef + e);
-        if (BATCH && m.y == out_l) c = make_double4(0.0, 0.0, 0.0, 0.0);  // outage
-        const int32_t jb = m.x;
-        const bool kside = (m.z & KSIDE) != 0;
-        const double th_j = y[A.y(jb)];
-        const double w = y[A.y(N + jb)];
-        const double u = v_i;
-        // thk = theta_h - theta_k (kernels.py:86)
-        const double thk = kside ? (th_j - th_i) : (th_i - th_j);
-        double si, ci;
-        pf_sincos(thk, tab, &si, &ci);
-        const double ab = u * w;
-        // h side: t1h = gl ci + bl si, t2h = gl si - bl ci.  k side with
-        // b1 = -bl2: t1k = gl2 ci - bl2 si, and t2s = -t2k.  Sign flips are
-        // exact, so every term below is bit-identical to kernels.py:90-163.
-        const double t1 = c.x * ci + c.y * si;
-        const double t2 = c.x * si - c.y * ci;
-        const double t2s = kside ? -t2 : t2;
-        const double fp = u * u * c.z - ab * t1;     // ph / pk
-        const double fq = -u * u * c.w - ab * t2s;   // qh / qk
-        acc_p -= fp;
-        acc_q -= fq;
-        if (MODE & JAC) {
-            d_pt += -ab * t2s;                     // gph_thh | gpk_thk
-            d_pv += -(2.0 * u * c.z - w * t1);     // gph_vh  | gpk_vk
-            d_qt += ab * t1;                       // gqh_thh | gqk_thk
-            d_qv += 2.0 * u * c.w + w * t2s;       // gqh_vh  | gqk_vk
-            const bool first = (m.z & FIRST) != 0;
-            const int64_t pos = m.z & POS_MASK;
-            put_offdiag<MODE>(jv, A.j(rp + pos), first, ab * t2s);        // gph_thk | gpk_thh
-            put_offdiag<MODE>(jv, A.j(rp + nb + pos), first, u * t1);     // gph_vk  | gpk_vh
-            put_offdiag<MODE>(jv, A.j(rq + pos), first, -ab * t1);        // gqh_thk | gqk_thh
-            put_offdiag<MODE>(jv, A.j(rq + nb + pos), first, u * t2s);    // gqh_vk  | gqk_vh
-        }
+        const double tj = y[m.x * S];
+        const double wj = y[(N + m.x) * S];
+        incidence<MODE, S>(tab, m, ldg4(d.inc_coef + e), th_i, v_i, tj, wj, out_l, jv, rp, rq,
+                           nb, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
     }
 
     // devices in pool-segment order: PQ, PV, Slack, Shunt (residual.py:57, 91-109)
-    const int32_t t1e = __ldg(d.dev_ptr + i + 1);
-    for (int32_t t = __ldg(d.dev_ptr + i); t < t1e; ++t) {
+    for (int32_t t = rng.z; t < rng.w; ++t) {
         const int4 dv = __ldg(d.dev_list + t);
         const int32_t k = dv.y;
         if (dv.x == DEV_PQ) {
-            const double p0 = (BATCH && pq_p) ? pq_p[A.pq(k)] : __ldg(d.pq_p0 + k);
-            const double q0 = (BATCH && pq_q) ? pq_q[A.pq(k)] : __ldg(d.pq_q0 + k);
+            const double p0 = (BATCH && A.pq_p) ? A.pq_p[k * S + ln] : __ldg(d.pq_p0 + k);
+            const double q0 = (BATCH && A.pq_q) ? A.pq_q[k * S + ln] : __ldg(d.pq_q0 + k);
             acc_p += -p0;
             acc_q += -q0;
         } else if (dv.x == DEV_PV) {
-            const double p0 = (BATCH && pv_p) ? pv_p[A.pv(k)] : __ldg(d.pv_p0 + k);
+            const double p0 = (BATCH && A.pv_p) ? A.pv_p[k * S + ln] : __ldg(d.pv_p0 + k);
             const int32_t q = __ldg(d.pv_qg + k);
-            const int64_t row = 2 * (int64_t)N + q;
+            const int32_t row = 2 * N + q;
             acc_p += p0;
-            acc_q += y[A.y(row)];
+            acc_q += y[row * S];
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - __ldg(d.pv_v0 + k));
-                if (MODE & RES) g[A.y(row)] = gv;
+                if (MODE & RES) st_out(A.g + ln + row * S, gv);
                 nrm = max(nrm, abs_bits(gv));
             }
             if (MODE & JAC) {
-                jv[A.j(dv.z)] = 1.0;   // (g_q[i], Q_g)   kernels.py:244-247
-                jv[A.j(dv.w)] = 1.0;   // (g_V, V_i)
+                st_out(jv + dv.z * S, 1.0);   // (g_q[i], Q_g)   kernels.py:244-247
+                st_out(jv + dv.w * S, 1.0);   // (g_V, V_i)
             }
         } else if (dv.x == DEV_SLACK) {
             const int32_t q = __ldg(d.sl_qg + k);
             const int32_t ps = __ldg(d.sl_ps + k);
-            const int64_t row_v = 2 * (int64_t)N + q;
-            const int64_t row_t = 2 * (int64_t)N + d.n_gen + ps;
-            acc_p += y[A.y(row_t)];
-            acc_q += y[A.y(row_v)];
+            const int32_t row_v = 2 * N + q;
+            const int32_t row_t = 2 * N + d.n_gen + ps;
+            acc_p += y[row_t * S];
+            acc_q += y[row_v * S];
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - __ldg(d.sl_v0 + k));
                 const double gt = 0.0 + (th_i - __ldg(d.sl_th0 + k));
                 if (MODE & RES) {
-                    g[A.y(row_v)] = gv;
-                    g[A.y(row_t)] = gt;
+                    st_out(A.g + ln + row_v * S, gv);
+                    st_out(A.g + ln + row_t * S, gt);
                 }
                 nrm = max(nrm, max(abs_bits(gv), abs_bits(gt)));
             }
             if (MODE & JAC) {
-                jv[A.j(dv.z)] = 1.0;                                   // (g_p, P_s)
-                jv[A.j(dv.w)] = 1.0;                                   // (g_q, Q_g)
-                jv[A.j(__ldg(d.gen_row_pos + q))] = 1.0;               // (g_V, V)
-                jv[A.j(__ldg(d.gen_row_pos + d.n_gen + ps))] = 1.0;    // (g_theta, theta)
+                st_out(jv + dv.z * S, 1.0);                                   // (g_p, P_s)
+                st_out(jv + dv.w * S, 1.0);                                   // (g_q, Q_g)
+                st_out(jv + __ldg(d.gen_row_pos + q) * S, 1.0);               // (g_V, V)
+                st_out(jv + __ldg(d.gen_row_pos + d.n_gen + ps) * S, 1.0);    // (g_theta, theta)
             }
         } else {  // DEV_SHUNT (kernels.py:236-241, 258-262)
             const double gsh = __ldg(d.sh_g + k), bsh = __ldg(d.sh_b + k);
@@ -188,58 +222,95 @@ __device__ __forceinline__ unsigned long long eval_bus(
     }
 
     if (MODE & RES) {
-        g[A.y(i)] = acc_p;
-        g[A.y(N + i)] = acc_q;
+        st_out(A.g + ln + i * S, acc_p);
+        st_out(A.g + ln + (N + i) * S, acc_q);
     }
     nrm = max(nrm, max(abs_bits(acc_p), abs_bits(acc_q)));
     if (MODE & JAC) {
         if (nb > 0) {
-            jv[A.j(rp + pos_i)] = d_pt;
-            jv[A.j(rq + pos_i)] = d_qt;
+            st_out(jv + (rp + pos_i) * S, d_pt);
+            st_out(jv + (rq + pos_i) * S, d_qt);
         }
         if (vdiag) {
-            jv[A.j(rp + nb + pos_i)] = d_pv;
-            jv[A.j(rq + nb + pos_i)] = d_qv;
+            st_out(jv + (rp + nb + pos_i) * S, d_pv);
+            st_out(jv + (rq + nb + pos_i) * S, d_qv);
         }
     }
     return nrm;
 }
 
-// Batched: blockDim = 32 * W, warp w of block (x, y) = bus x*W + w of
-// scenario block y; lane = scenario within the block.
-template <int MODE, int W>
-__global__ void __launch_bounds__(32 * W) k_eval_batched(
-    const DevicePlan d, const int32_t K, const double* __restrict__ y,
-    const double* __restrict__ pq_p, const double* __restrict__ pq_q,
-    const double* __restrict__ pv_p, const int32_t* __restrict__ outage,
-    double* __restrict__ g, double* __restrict__ jv, unsigned long long* __restrict__ norms) {
+// Batched, persistent: gridDim.x CTAs (a few per SM) stride over work items
+// (scenario block b, group of W buses) in block-major order, so the whole
+// GPU sweeps one 32-scenario block at a time and its states stay in L2.
+// Warp w of an item evaluates bus (group * W + w) for the block's 32
+// scenarios (lane = scenario).  Norms: per-lane running max per block,
+// reduced across the CTA's warps and atomically max-ed into norms[s] only
+// when the CTA moves to the next block (integer max of |g| bit patterns is
+// exact and order-independent, NaN-propagating like numpy).
+template <int MODE, int W, int MINB, int U>
+__global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
+    const DevicePlan d, const int32_t K, const int32_t n_groups, const int32_t n_items,
+    const double* __restrict__ y, const double* __restrict__ pq_p,
+    const double* __restrict__ pq_q, const double* __restrict__ pv_p,
+    const int32_t* __restrict__ outage, double* __restrict__ g, double* __restrict__ jv,
+    unsigned long long* __restrict__ norms) {
     __shared__ unsigned long long red[W][32];
     __shared__ double s_tab[PF_TRIG_N * 4];
     const double* tab = stage_trig_table(s_tab);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t bus = blockIdx.x * W + warp;
-    const int64_t blk = blockIdx.y;
-    const int32_t s = (int32_t)(blk * PF_LANES + lane);
+    int32_t cur = -1;
     unsigned long long nrm = 0;
-    if (bus < d.N && s < K) {
-        Addr<true> A;
-        A.y0 = blk * (int64_t)d.n_var * PF_LANES + lane;
-        A.j0 = blk * (int64_t)d.nnz * PF_LANES + lane;
-        A.pq0 = blk * (int64_t)d.P * PF_LANES + lane;
-        A.pv0 = blk * (int64_t)d.G * PF_LANES + lane;
-        const int32_t out_l = outage ? __ldg(outage + s) : -1;
-        nrm = eval_bus<MODE, true>(d, tab, bus, A, out_l, y, pq_p, pq_q, pv_p, g, jv);
-    }
-    if (MODE & NORM) {
-        red[warp][lane] = nrm;
-        __syncthreads();
-        if (warp == 0) {
-            unsigned long long m = red[0][lane];
+    auto flush = [&](int32_t blk) {
+        __syncthreads();  // every warp is done with the previous block
+        if (MODE & NORM) {
+            red[warp][lane] = nrm;
+            __syncthreads();
+            if (warp == 0) {
+                unsigned long long mx = red[0][lane];
 #pragma unroll
-            for (int w = 1; w < W; ++w) m = max(m, red[w][lane]);
-            if (s < K && m) atomicMax(norms + s, m);
+                for (int w = 1; w < W; ++w) mx = max(mx, red[w][lane]);
+                const int32_t s = blk * PF_LANES + lane;
+                if (s < K && mx) atomicMax(norms + s, mx);
+            }
+            __syncthreads();
+        }
+        nrm = 0;
+    };
+    // item = blk * n_groups + grp, walked with a stride of gridDim.x
+    // (gridDim.x <= n_groups, so grp wraps at most once per step)
+    int32_t blk = blockIdx.x / n_groups;
+    int32_t grp = blockIdx.x - blk * n_groups;
+    // block base pointers live in shared memory (one copy per CTA) so they
+    // cost no registers across the incidence loop
+    __shared__ Scen<PF_LANES> A;
+    int32_t out_l = -1;
+    for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        if (blk != cur) {
+            if (cur >= 0) flush(cur);
+            cur = blk;
+            if (threadIdx.x == 0) {
+                const int64_t b = blk;
+                A.y = y + b * d.n_var * PF_LANES;
+                A.g = g ? g + b * d.n_var * PF_LANES : nullptr;
+                A.j = jv ? jv + b * d.nnz * PF_LANES : nullptr;
+                A.pq_p = pq_p ? pq_p + b * d.P * PF_LANES : nullptr;
+                A.pq_q = pq_q ? pq_q + b * d.P * PF_LANES : nullptr;
+                A.pv_p = pv_p ? pv_p + b * d.G * PF_LANES : nullptr;
+            }
+            const int32_t s = blk * PF_LANES + lane;
+            out_l = (outage && s < K) ? __ldg(outage + s) : -1;
+            __syncthreads();
+        }
+        const int32_t bus = grp * W + warp;
+        if (bus < d.N && blk * PF_LANES + lane < K)
+            nrm = max(nrm, eval_bus<MODE, PF_LANES, U>(d, tab, bus, A, lane, out_l));
+        grp += gridDim.x;
+        while (grp >= n_groups) {
+            grp -= n_groups;
+            ++blk;
         }
     }
+    if (cur >= 0) flush(cur);
 }
 
 template <int MODE>
@@ -254,8 +325,8 @@ __global__ void __launch_bounds__(128) k_eval_single(const DevicePlan d,
     const int32_t bus = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long nrm = 0;
     if (bus < d.N) {
-        Addr<false> A{0, 0, 0, 0};
-        nrm = eval_bus<MODE, false>(d, tab, bus, A, -1, y, nullptr, nullptr, nullptr, g, jv);
+        Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
+        nrm = eval_bus<MODE, 1, 1>(d, tab, bus, A, 0, -1);
     }
     if (MODE & NORM) {
         for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
@@ -487,14 +558,57 @@ cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, 
 
 constexpr int BATCH_W = 8;
 
+template <int MODE, int MINB, int U>
+static cudaError_t launch_batched_minb(const DevicePlan& d, int32_t K, const double* y,
+                                       const double* pq_p, const double* pq_q,
+                                       const double* pv_p, const int32_t* outage, double* g,
+                                       double* j, double* norms, cudaStream_t st) {
+    static int ctas = 0;  // resident CTAs per SM for this instantiation
+    static int sms = 0;
+    if (!ctas) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, k_eval_batched<MODE, BATCH_W, MINB, U>,
+                                                      32 * BATCH_W, 0);
+        if (ctas < 1) ctas = 1;
+        if (const char* g = getenv("PFGPU_GRID_CTAS")) ctas = atoi(g);
+    }
+    const int32_t n_groups = (d.N + BATCH_W - 1) / BATCH_W;
+    const int64_t n_items64 = (int64_t)n_groups * ((K + PF_LANES - 1) / PF_LANES);
+    if (n_items64 >= (1ll << 31)) return cudaErrorInvalidValue;
+    const int32_t n_items = (int32_t)n_items64;
+    const int grid = (int)std::min<int64_t>(std::min<int64_t>(n_items, n_groups),
+                                            (int64_t)ctas * sms);
+    k_eval_batched<MODE, BATCH_W, MINB, U><<<grid, 32 * BATCH_W, 0, st>>>(
+        d, K, n_groups, n_items, y, pq_p, pq_q, pv_p, outage, g, j,
+        reinterpret_cast<unsigned long long*>(norms));
+    return cudaSuccess;
+}
+
 template <int MODE>
-static void launch_batched_mode(const DevicePlan& d, int32_t K, const double* y,
-                                const double* pq_p, const double* pq_q, const double* pv_p,
-                                const int32_t* outage, double* g, double* j, double* norms,
-                                cudaStream_t st) {
-    dim3 grid(grid_for(d.N, BATCH_W), grid_for(K, PF_LANES));
-    k_eval_batched<MODE, BATCH_W><<<grid, 32 * BATCH_W, 0, st>>>(
-        d, K, y, pq_p, pq_q, pv_p, outage, g, j, reinterpret_cast<unsigned long long*>(norms));
+static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const double* y,
+                                       const double* pq_p, const double* pq_q,
+                                       const double* pv_p, const int32_t* outage, double* g,
+                                       double* j, double* norms, cudaStream_t st) {
+    static int variant = -1;
+    if (variant < 0) {
+        const char* e = getenv("PFGPU_VARIANT");
+        variant = e ? atoi(e) : 13;
+    }
+    if (variant == 99 && MODE == (RES | JAC | NORM))
+        return launch_batched_minb<RES | JAC | NORM | CHEAP_TRIG, 3, 1>(d, K, y, pq_p, pq_q, pv_p,
+                                                                      outage, g, j, norms, st);
+#define PF_V(MB, U) launch_batched_minb<MODE, MB, U>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st)
+    switch (variant) {
+        case 12: return PF_V(2, 1);
+        case 14: return PF_V(4, 1);
+        case 22: return PF_V(2, 2);
+        case 23: return PF_V(3, 2);
+        case 24: return PF_V(2, 4);
+        default: return PF_V(3, 1);
+    }
+#undef PF_V
 }
 
 cudaError_t launch_eval_batched(const DevicePlan& d, int32_t K, const double* y,
@@ -508,16 +622,18 @@ cudaError_t launch_eval_batched(const DevicePlan& d, int32_t K, const double* y,
     if (d.N == 0 || K == 0) return cudaSuccess;
     const int mode = (g ? RES : 0) | (j ? JAC : 0) | (norms ? NORM : 0);
 #define PF_B(M) launch_batched_mode<M>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st)
+    cudaError_t e = cudaSuccess;
     switch (mode) {
-        case RES: PF_B(RES); break;
-        case JAC: PF_B(JAC); break;
-        case RES | JAC: PF_B(RES | JAC); break;
-        case NORM: PF_B(NORM); break;
-        case RES | NORM: PF_B(RES | NORM); break;
-        case JAC | NORM: PF_B(JAC | NORM); break;
-        case RES | JAC | NORM: PF_B(RES | JAC | NORM); break;
+        case RES: e = PF_B(RES); break;
+        case JAC: e = PF_B(JAC); break;
+        case RES | JAC: e = PF_B(RES | JAC); break;
+        case NORM: e = PF_B(NORM); break;
+        case RES | NORM: e = PF_B(RES | NORM); break;
+        case JAC | NORM: e = PF_B(JAC | NORM); break;
+        case RES | JAC | NORM: e = PF_B(RES | JAC | NORM); break;
         default: return cudaSuccess;
     }
+    if (e != cudaSuccess) return e;
 #undef PF_B
     count_launch();
     return cudaGetLastError();

@@ -249,7 +249,8 @@ __global__ void k_fill(int32_t N, int32_t n_gen, const int32_t* ubase, const int
         }
         dev_list[u] = ent;
     }
-    bus_row[i] = make_int4((int32_t)rp, (int32_t)rq, nb, pos_i[i] | (nv > 0 ? VDIAG : 0));
+    bus_row[2 * i] = make_int4((int32_t)rp, (int32_t)rq, nb, pos_i[i] | (nv > 0 ? VDIAG : 0));
+    bus_row[2 * i + 1] = make_int4(inc_ptr[i], inc_ptr[i + 1], dev_ptr[i], dev_ptr[i + 1]);
 }
 
 __global__ void k_csr_keys(int32_t n, const int64_t* indptr, const int32_t* indices,
@@ -545,7 +546,7 @@ int build(const pf_topology* t, pf_plan** out) {
     int32_t* gen_row_pos;
     PF_TRY(owned_alloc(P, &indices, d.nnz));
     PF_TRY(owned_alloc(P, &indptr, n_var + 1));
-    PF_TRY(owned_alloc(P, &bus_row, N));
+    PF_TRY(owned_alloc(P, &bus_row, 2 * (int64_t)N));
     PF_TRY(owned_alloc(P, &dev_list, n_dev));
     PF_TRY(owned_alloc(P, &gen_row_pos, d.n_gen + d.S));
     if (N)

@@ -42,6 +42,16 @@
 #define PF_C4 (1.0 / 24.0)
 #define PF_C6 (-1.0 / 720.0)
 
+#ifdef __CUDACC__
+/* huge / non-finite arguments: out of line so the hot path stays small;
+ * returned by value so the caller needs no stack slot */
+__device__ __noinline__ static double2 pf_sincos_slow(double x) {
+    double2 r;
+    sincos(x, &r.x, &r.y);
+    return r;
+}
+#endif
+
 PF_HD void pf_two_sum(double a, double b, double* s, double* e) {
     double ss = a + b;
     double bb = ss - a;
@@ -54,26 +64,33 @@ PF_HD void pf_two_sum(double a, double b, double* s, double* e) {
 PF_HD void pf_sincos_tab(double x, const double* tab, double* sp, double* cp) {
     if (!(fabs(x) < 1048576.0)) {
 #ifdef __CUDA_ARCH__
-        sincos(x, sp, cp);
+        const double2 r = pf_sincos_slow(x);
+        *sp = r.x;
+        *cp = r.y;
 #else
         *sp = sin(x);
         *cp = cos(x);
 #endif
         return;
     }
-    /* 1. r = x - k pi/2 in double-double */
-    const double kf = rint(x * PF_TWO_OVER_PI);
-    const double ph = kf * PF_PIO2_1;
-    const double pl = fma(kf, PF_PIO2_1, -ph);
-    const double t = x - ph; /* exact (Sterbenz) */
-    const double qh = kf * PF_PIO2_2;
-    const double ql = fma(kf, PF_PIO2_2, -qh);
-    double s1, e1, s2, e2;
-    pf_two_sum(t, -pl, &s1, &e1);
-    pf_two_sum(s1, -qh, &s2, &e2);
-    const double rl0 = ((e1 + e2) - ql) - kf * PF_PIO2_3;
-    const double rh = s2 + rl0;
-    const double rl = rl0 - (rh - s2);
+    /* 1. r = x - k pi/2 in double-double.  |x| <= pi/4 (the usual power-flow
+     * angle difference) has k = 0, for which the reduction is the identity
+     * bit for bit, so it is skipped. */
+    double kf = 0.0, rh = x, rl = 0.0;
+    if (fabs(x) > 0.78539816339744828) {
+        kf = rint(x * PF_TWO_OVER_PI);
+        const double ph = kf * PF_PIO2_1;
+        const double pl = fma(kf, PF_PIO2_1, -ph);
+        const double t = x - ph; /* exact (Sterbenz) */
+        const double qh = kf * PF_PIO2_2;
+        const double ql = fma(kf, PF_PIO2_2, -qh);
+        double s1, e1, s2, e2;
+        pf_two_sum(t, -pl, &s1, &e1);
+        pf_two_sum(s1, -qh, &s2, &e2);
+        const double rl0 = ((e1 + e2) - ql) - kf * PF_PIO2_3;
+        rh = s2 + rl0;
+        rl = rl0 - (rh - s2);
+    }
     /* 2. |r| = X_i + d */
     const bool neg = rh < 0.0;
     const double a = fabs(rh);
@@ -82,19 +99,22 @@ PF_HD void pf_sincos_tab(double x, const double* tab, double* sp, double* cp) {
     const int i = (int)fi;
     const double dh = a - fi * 0.015625; /* exact */
     const double z = dh * dh;
-    const double sd = al + dh * z * (PF_S3 + z * (PF_S5 + z * PF_S7)); /* sin d - dh */
-    const double cm1 = z * (PF_C2 + z * (PF_C4 + z * PF_C6)) - dh * al; /* cos d - 1 */
+    /* sin d - dh and cos d - 1 (Horner with explicit FMAs) */
+    const double sd = fma(dh * z, fma(z, fma(z, PF_S7, PF_S5), PF_S3), al);
+    const double cm1 = fma(z, fma(z, fma(z, PF_C6, PF_C4), PF_C2), -(dh * al));
     const double Sh = tab[4 * i], Ch = tab[4 * i + 1], Sl = tab[4 * i + 2], Cl = tab[4 * i + 3];
-    /* 3. sin and cos of |r| */
-    double h, e;
+    /* 3. sin and cos of |r|: leading sum split exactly (Fast2Sum is valid:
+     * |Sh| >= |Ch dh| for i >= 1, and Sh = 0 for i = 0; |Ch| >= |Sh dh|) */
     const double P = Ch * dh;
     const double Pl = fma(Ch, dh, -P);
-    pf_two_sum(Sh, P, &h, &e);
-    double s = h + (e + (Pl + (Sl + (Ch * sd + (Cl * dh + Sh * cm1)))));
+    double h = Sh + P;
+    double e = P - (h - Sh);
+    double s = h + (e + (Pl + (Sl + fma(Ch, sd, fma(Cl, dh, Sh * cm1)))));
     const double Q = Sh * dh;
     const double Ql = fma(Sh, dh, -Q);
-    pf_two_sum(Ch, -Q, &h, &e);
-    const double c = h + (e + (-Ql + (Cl + (-(Sh * sd) + (-(Sl * dh) + Ch * cm1)))));
+    h = Ch - Q;
+    e = (Ch - h) - Q;
+    const double c = h + (e + (Cl - fma(Sh, sd, fma(Sl, dh, fma(-Ch, cm1, Ql)))));
     s = neg ? -s : s;
     /* 4. quadrant */
     const int q = (int)((long long)kf & 3);
