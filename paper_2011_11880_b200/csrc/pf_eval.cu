@@ -22,7 +22,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "pf_internal.cuh"
 #include "pf_trig.h"
@@ -30,7 +29,7 @@
 namespace pf {
 namespace {
 
-constexpr int RES = 1, JAC = 2, NORM = 4, CHEAP_TRIG = 8;  // CHEAP_TRIG: dev experiment only
+constexpr int RES = 1, JAC = 2, NORM = 4;
 
 // The one trig routine every kernel uses (fused, per-model, test surface):
 // near-correctly-rounded table sin/cos (pf_trig.h), table staged in shared
@@ -71,6 +70,56 @@ struct Scen {
     int32_t out_l;
 };
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Stage the next item of this warp: pull the scenario-block data bus `i`'s
+// evaluation will read (its own state, every neighbour's state, each
+// device's per-scenario parameters: 256 B = 2 lines per entry) from HBM into
+// L2 while the current item computes, and touch its incidence / device
+// records (real loads, so they land in L1).  The lanes split the incidence
+// and device lists, so one pass issues every line at once.  Measured on B200
+// (config 3): 0.778 -> 0.732 ms per K=256 launch; an L1 prefetch or a
+// two-items-ahead distance measured no better.
+template <int S>
+__device__ __forceinline__ void stage_next_bus(const DevicePlan& d, const Scen<S>& A,
+                                               const int32_t i, const int4 rng, const int lane) {
+    const int32_t N = d.N;
+    const double* y = A.y;
+    if (lane < 4) {
+        const int64_t e = (lane < 2) ? i : N + i;
+        prefetch_l2(y + e * S + (lane & 1) * 16);
+    }
+    for (int32_t e = rng.x + lane; e < rng.y; e += 32) {
+        const int32_t j = __ldg(&d.inc_meta[e].x);
+        prefetch_l2(y + (int64_t)j * S);
+        prefetch_l2(y + (int64_t)j * S + 16);
+        prefetch_l2(y + (int64_t)(N + j) * S);
+        prefetch_l2(y + (int64_t)(N + j) * S + 16);
+    }
+    for (int32_t t = rng.z + lane; t < rng.w; t += 32) {
+        const int4 dv = __ldg(d.dev_list + t);
+        const double* a = nullptr;
+        const double* b = nullptr;
+        if (dv.x == DEV_PQ) {
+            a = A.pq_p ? A.pq_p + (int64_t)dv.y * S : nullptr;
+            b = A.pq_q ? A.pq_q + (int64_t)dv.y * S : nullptr;
+        } else if (dv.x == DEV_PV) {
+            a = A.pv_p ? A.pv_p + (int64_t)dv.y * S : nullptr;
+            b = y + (int64_t)(2 * N + __ldg(d.pv_qg + dv.y)) * S;
+        }
+        if (a) {
+            prefetch_l2(a);
+            prefetch_l2(a + 16);
+        }
+        if (b) {
+            prefetch_l2(b);
+            prefetch_l2(b + 16);
+        }
+    }
+}
+
 // Outputs are written once and never re-read by the kernel (except the rare
 // parallel-branch update), so store them evict-first: the 2.3 GB/step output
 // stream must not push the scenario states out of L2.
@@ -101,12 +150,7 @@ __device__ __forceinline__ void incidence(const double* tab, const int4 m, doubl
     // thk = theta_h - theta_k (kernels.py:86)
     const double thk = kside ? (th_j - th_i) : (th_i - th_j);
     double si, ci;
-    if (MODE & CHEAP_TRIG) {
-        si = thk;
-        ci = 1.0 - thk;
-    } else {
-        pf_sincos(thk, tab, &si, &ci);
-    }
+    pf_sincos(thk, tab, &si, &ci);
     const double ab = u * w;
     // h side: t1h = gl ci + bl si, t2h = gl si - bl ci.  k side with
     // b1 = -bl2: t1k = gl2 ci - bl2 si, and t2s = -t2k.  Sign flips are
@@ -132,9 +176,7 @@ __device__ __forceinline__ void incidence(const double* tab, const int4 m, doubl
 }
 
 // One bus for one scenario (S = PF_LANES: batched lane; S = 1: single grid).
-// U incidences are fetched together (metadata + neighbour states) before
-// their arithmetic runs in list order, so U gathers are in flight at once.
-template <int MODE, int S, int U>
+template <int MODE, int S>
 __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, const double* tab,
                                                        const int32_t i, const Scen<S>& A,
                                                        const int32_t ln, const int32_t out_l) {
@@ -148,8 +190,8 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
     const int32_t pos_i = br.w & POS_MASK;
     const bool vdiag = (br.w & VDIAG) != 0;
     const int32_t e0 = rng.x, e1 = rng.y;
-    const double th_i = y[i * S];
-    const double v_i = y[(N + i) * S];
+    const double th_i = __ldg(y + (i * S));
+    const double v_i = __ldg(y + ((N + i) * S));
 
     double acc_p = 0.0, acc_q = 0.0;
     double d_pt = 0.0, d_pv = 0.0, d_qt = 0.0, d_qv = 0.0;
@@ -157,8 +199,8 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
 
     for (int32_t e = e0; e < e1; ++e) {
         const int4 m = __ldg(d.inc_meta + e);
-        const double tj = y[m.x * S];
-        const double wj = y[(N + m.x) * S];
+        const double tj = __ldg(y + (m.x * S));
+        const double wj = __ldg(y + ((N + m.x) * S));
         incidence<MODE, S>(tab, m, ldg4(d.inc_coef + e), th_i, v_i, tj, wj, out_l, jv, rp, rq,
                            nb, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
     }
@@ -168,16 +210,16 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
         const int4 dv = __ldg(d.dev_list + t);
         const int32_t k = dv.y;
         if (dv.x == DEV_PQ) {
-            const double p0 = (BATCH && A.pq_p) ? A.pq_p[k * S + ln] : __ldg(d.pq_p0 + k);
-            const double q0 = (BATCH && A.pq_q) ? A.pq_q[k * S + ln] : __ldg(d.pq_q0 + k);
+            const double p0 = (BATCH && A.pq_p) ? __ldg(A.pq_p + k * S + ln) : __ldg(d.pq_p0 + k);
+            const double q0 = (BATCH && A.pq_q) ? __ldg(A.pq_q + k * S + ln) : __ldg(d.pq_q0 + k);
             acc_p += -p0;
             acc_q += -q0;
         } else if (dv.x == DEV_PV) {
-            const double p0 = (BATCH && A.pv_p) ? A.pv_p[k * S + ln] : __ldg(d.pv_p0 + k);
+            const double p0 = (BATCH && A.pv_p) ? __ldg(A.pv_p + k * S + ln) : __ldg(d.pv_p0 + k);
             const int32_t q = __ldg(d.pv_qg + k);
             const int32_t row = 2 * N + q;
             acc_p += p0;
-            acc_q += y[row * S];
+            acc_q += __ldg(y + (row * S));
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - __ldg(d.pv_v0 + k));
                 if (MODE & RES) st_out(A.g + ln + row * S, gv);
@@ -192,8 +234,8 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
             const int32_t ps = __ldg(d.sl_ps + k);
             const int32_t row_v = 2 * N + q;
             const int32_t row_t = 2 * N + d.n_gen + ps;
-            acc_p += y[row_t * S];
-            acc_q += y[row_v * S];
+            acc_p += __ldg(y + (row_t * S));
+            acc_q += __ldg(y + (row_v * S));
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - __ldg(d.sl_v0 + k));
                 const double gt = 0.0 + (th_i - __ldg(d.sl_th0 + k));
@@ -247,7 +289,7 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
 // reduced across the CTA's warps and atomically max-ed into norms[s] only
 // when the CTA moves to the next block (integer max of |g| bit patterns is
 // exact and order-independent, NaN-propagating like numpy).
-template <int MODE, int W, int MINB, int U>
+template <int MODE, int W, int MINB>
 __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
     const DevicePlan d, const int32_t K, const int32_t n_groups, const int32_t n_items,
     const double* __restrict__ y, const double* __restrict__ pq_p,
@@ -302,8 +344,15 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
             __syncthreads();
         }
         const int32_t bus = grp * W + warp;
+        // stage the next item of this warp (same block only) behind this one
+        const int32_t gn = grp + gridDim.x;
+        const int32_t bn = gn * W + warp;
+        const bool pre = gn < n_groups && bn < d.N;
+        int4 rng_n = make_int4(0, 0, 0, 0);
+        if (pre) rng_n = __ldg(d.bus_row + 2 * bn + 1);
         if (bus < d.N && blk * PF_LANES + lane < K)
-            nrm = max(nrm, eval_bus<MODE, PF_LANES, U>(d, tab, bus, A, lane, out_l));
+            nrm = max(nrm, eval_bus<MODE, PF_LANES>(d, tab, bus, A, lane, out_l));
+        if (pre) stage_next_bus<PF_LANES>(d, A, bn, rng_n, lane);
         grp += gridDim.x;
         while (grp >= n_groups) {
             grp -= n_groups;
@@ -326,7 +375,7 @@ __global__ void __launch_bounds__(128) k_eval_single(const DevicePlan d,
     unsigned long long nrm = 0;
     if (bus < d.N) {
         Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
-        nrm = eval_bus<MODE, 1, 1>(d, tab, bus, A, 0, -1);
+        nrm = eval_bus<MODE, 1>(d, tab, bus, A, 0, -1);
     }
     if (MODE & NORM) {
         for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
@@ -558,8 +607,13 @@ cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, 
 
 constexpr int BATCH_W = 8;
 
-template <int MODE, int MINB, int U>
-static cudaError_t launch_batched_minb(const DevicePlan& d, int32_t K, const double* y,
+// 8 warps per CTA, 3 CTAs per SM (80 registers, no spills).  Measured
+// alternatives on B200: 2 CTAs (more registers) and 4 CTAs (64 registers,
+// spills) were both slower.
+constexpr int BATCH_MINB = 3;
+
+template <int MODE>
+static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const double* y,
                                        const double* pq_p, const double* pq_q,
                                        const double* pv_p, const int32_t* outage, double* g,
                                        double* j, double* norms, cudaStream_t st) {
@@ -569,10 +623,9 @@ static cudaError_t launch_batched_minb(const DevicePlan& d, int32_t K, const dou
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, k_eval_batched<MODE, BATCH_W, MINB, U>,
-                                                      32 * BATCH_W, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &ctas, k_eval_batched<MODE, BATCH_W, BATCH_MINB>, 32 * BATCH_W, 0);
         if (ctas < 1) ctas = 1;
-        if (const char* g = getenv("PFGPU_GRID_CTAS")) ctas = atoi(g);
     }
     const int32_t n_groups = (d.N + BATCH_W - 1) / BATCH_W;
     const int64_t n_items64 = (int64_t)n_groups * ((K + PF_LANES - 1) / PF_LANES);
@@ -580,35 +633,10 @@ static cudaError_t launch_batched_minb(const DevicePlan& d, int32_t K, const dou
     const int32_t n_items = (int32_t)n_items64;
     const int grid = (int)std::min<int64_t>(std::min<int64_t>(n_items, n_groups),
                                             (int64_t)ctas * sms);
-    k_eval_batched<MODE, BATCH_W, MINB, U><<<grid, 32 * BATCH_W, 0, st>>>(
+    k_eval_batched<MODE, BATCH_W, BATCH_MINB><<<grid, 32 * BATCH_W, 0, st>>>(
         d, K, n_groups, n_items, y, pq_p, pq_q, pv_p, outage, g, j,
         reinterpret_cast<unsigned long long*>(norms));
     return cudaSuccess;
-}
-
-template <int MODE>
-static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const double* y,
-                                       const double* pq_p, const double* pq_q,
-                                       const double* pv_p, const int32_t* outage, double* g,
-                                       double* j, double* norms, cudaStream_t st) {
-    static int variant = -1;
-    if (variant < 0) {
-        const char* e = getenv("PFGPU_VARIANT");
-        variant = e ? atoi(e) : 13;
-    }
-    if (variant == 99 && MODE == (RES | JAC | NORM))
-        return launch_batched_minb<RES | JAC | NORM | CHEAP_TRIG, 3, 1>(d, K, y, pq_p, pq_q, pv_p,
-                                                                      outage, g, j, norms, st);
-#define PF_V(MB, U) launch_batched_minb<MODE, MB, U>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st)
-    switch (variant) {
-        case 12: return PF_V(2, 1);
-        case 14: return PF_V(4, 1);
-        case 22: return PF_V(2, 2);
-        case 23: return PF_V(3, 2);
-        case 24: return PF_V(2, 4);
-        default: return PF_V(3, 1);
-    }
-#undef PF_V
 }
 
 cudaError_t launch_eval_batched(const DevicePlan& d, int32_t K, const double* y,

@@ -72,7 +72,7 @@ struct Staging {
 struct pf_plan {
     pf::DevicePlan d;
     int32_t max_deg = 0;
-    void* owned[64] = {};   // device allocations to free
+    void* owned[96] = {};   // device allocations to free
     int n_owned = 0;
     // single-grid host drop-in staging
     double *s_y = nullptr, *s_g = nullptr, *s_j = nullptr, *s_jc = nullptr, *s_norm = nullptr;
