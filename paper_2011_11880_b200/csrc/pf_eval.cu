@@ -145,7 +145,10 @@ __device__ __forceinline__ void incidence(const double* tab, const int4 m, doubl
                                           double& acc_q, double& d_pt, double& d_pv,
                                           double& d_qt, double& d_qv) {
     constexpr bool BATCH = S > 1;
-    if (BATCH && m.y == out_l) c = make_double4(0.0, 0.0, 0.0, 0.0);  // outage
+    if (BATCH) {  // outaged branch in some lane's scenario: rare, so test warp-wide first
+        const bool hit = m.y == out_l;
+        if (__any_sync(__activemask(), hit) && hit) c = make_double4(0.0, 0.0, 0.0, 0.0);
+    }
     const bool kside = (m.z & KSIDE) != 0;
     // thk = theta_h - theta_k (kernels.py:86)
     const double thk = kside ? (th_j - th_i) : (th_i - th_j);
@@ -175,51 +178,83 @@ __device__ __forceinline__ void incidence(const double* tab, const int4 m, doubl
     }
 }
 
-// One bus for one scenario (S = PF_LANES: batched lane; S = 1: single grid).
-template <int MODE, int S>
-__device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, const double* tab,
-                                                       const int32_t i, const Scen<S>& A,
-                                                       const int32_t ln, const int32_t out_l) {
-    constexpr bool BATCH = S > 1;
+// Operand source of the global-memory path: every read goes to HBM/L2/L1.
+template <int S>
+struct GlobalSrc {
+    const DevicePlan& d;
+    const Scen<S>& A;               // block base pointers (shared memory when batched)
+    const double* __restrict__ y;   // this lane's scenario view of the state
+    int32_t i, ln;
+    __device__ __forceinline__ int4 hdr0() const { return __ldg(d.bus_row + 2 * i); }
+    __device__ __forceinline__ int4 hdr1() const { return __ldg(d.bus_row + 2 * i + 1); }
+    __device__ __forceinline__ double th_i() const { return __ldg(y + i * S); }
+    __device__ __forceinline__ double v_i() const { return __ldg(y + (d.N + i) * S); }
+    __device__ __forceinline__ int4 meta(int32_t e, int32_t) const { return __ldg(d.inc_meta + e); }
+    __device__ __forceinline__ double4 coef(int32_t e, int32_t) const { return ldg4(d.inc_coef + e); }
+    __device__ __forceinline__ double th_j(int32_t j, int32_t) const { return __ldg(y + j * S); }
+    __device__ __forceinline__ double v_j(int32_t j, int32_t) const {
+        return __ldg(y + (d.N + j) * S);
+    }
+    __device__ __forceinline__ int4 dev(int32_t t, int32_t) const { return __ldg(d.dev_list + t); }
+    // per-scenario device operands: (a, b) = PQ (p0, q0), PV (p0, Q_g), Slack (P_s, Q_g)
+    __device__ __forceinline__ double dev_a(const int4 dv, int32_t) const {
+        const int32_t k = dv.y;
+        if (dv.x == DEV_PQ)
+            return (S > 1 && A.pq_p) ? __ldg(A.pq_p + k * S + ln) : __ldg(d.pq_p0 + k);
+        if (dv.x == DEV_PV)
+            return (S > 1 && A.pv_p) ? __ldg(A.pv_p + k * S + ln) : __ldg(d.pv_p0 + k);
+        return __ldg(y + (2 * d.N + d.n_gen + __ldg(d.sl_ps + k)) * S);
+    }
+    __device__ __forceinline__ double dev_b(const int4 dv, int32_t) const {
+        const int32_t k = dv.y;
+        if (dv.x == DEV_PQ)
+            return (S > 1 && A.pq_q) ? __ldg(A.pq_q + k * S + ln) : __ldg(d.pq_q0 + k);
+        if (dv.x == DEV_PV) return __ldg(y + (2 * d.N + __ldg(d.pv_qg + k)) * S);
+        return __ldg(y + (2 * d.N + __ldg(d.sl_qg + k)) * S);
+    }
+};
+
+// One bus for one scenario (S = PF_LANES: batched lane; S = 1: single grid),
+// operands from `src` (global memory or a shared-memory staging slot).
+template <int MODE, int S, class Src>
+__device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, const double* tab,
+                                                           const int32_t i, const Src& src,
+                                                           const Scen<S>& A, const int32_t ln,
+                                                           const int32_t out_l) {
     const int32_t N = d.N;
-    const double* __restrict__ y = A.y + ln;
     double* __restrict__ jv = A.j ? A.j + ln : nullptr;
-    const int4 br = __ldg(d.bus_row + 2 * i);
-    const int4 rng = __ldg(d.bus_row + 2 * i + 1);
+    const int4 br = src.hdr0();
+    const int4 rng = src.hdr1();
     const int32_t rp = br.x, rq = br.y, nb = br.z;
     const int32_t pos_i = br.w & POS_MASK;
     const bool vdiag = (br.w & VDIAG) != 0;
-    const int32_t e0 = rng.x, e1 = rng.y;
-    const double th_i = __ldg(y + (i * S));
-    const double v_i = __ldg(y + ((N + i) * S));
+    const double th_i = src.th_i();
+    const double v_i = src.v_i();
 
     double acc_p = 0.0, acc_q = 0.0;
     double d_pt = 0.0, d_pv = 0.0, d_qt = 0.0, d_qv = 0.0;
     unsigned long long nrm = 0;
 
-    for (int32_t e = e0; e < e1; ++e) {
-        const int4 m = __ldg(d.inc_meta + e);
-        const double tj = __ldg(y + (m.x * S));
-        const double wj = __ldg(y + ((N + m.x) * S));
-        incidence<MODE, S>(tab, m, ldg4(d.inc_coef + e), th_i, v_i, tj, wj, out_l, jv, rp, rq,
-                           nb, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
+    for (int32_t e = rng.x; e < rng.y; ++e) {
+        const int32_t t = e - rng.x;
+        const int4 m = src.meta(e, t);
+        const double tj = src.th_j(m.x, t);
+        const double wj = src.v_j(m.x, t);
+        incidence<MODE, S>(tab, m, src.coef(e, t), th_i, v_i, tj, wj, out_l, jv, rp, rq, nb,
+                           acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
     }
 
     // devices in pool-segment order: PQ, PV, Slack, Shunt (residual.py:57, 91-109)
     for (int32_t t = rng.z; t < rng.w; ++t) {
-        const int4 dv = __ldg(d.dev_list + t);
+        const int4 dv = src.dev(t, t - rng.z);
         const int32_t k = dv.y;
         if (dv.x == DEV_PQ) {
-            const double p0 = (BATCH && A.pq_p) ? __ldg(A.pq_p + k * S + ln) : __ldg(d.pq_p0 + k);
-            const double q0 = (BATCH && A.pq_q) ? __ldg(A.pq_q + k * S + ln) : __ldg(d.pq_q0 + k);
-            acc_p += -p0;
-            acc_q += -q0;
+            acc_p += -src.dev_a(dv, t - rng.z);
+            acc_q += -src.dev_b(dv, t - rng.z);
         } else if (dv.x == DEV_PV) {
-            const double p0 = (BATCH && A.pv_p) ? __ldg(A.pv_p + k * S + ln) : __ldg(d.pv_p0 + k);
-            const int32_t q = __ldg(d.pv_qg + k);
-            const int32_t row = 2 * N + q;
-            acc_p += p0;
-            acc_q += __ldg(y + (row * S));
+            const int32_t row = 2 * N + __ldg(d.pv_qg + k);
+            acc_p += src.dev_a(dv, t - rng.z);
+            acc_q += src.dev_b(dv, t - rng.z);
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - __ldg(d.pv_v0 + k));
                 if (MODE & RES) st_out(A.g + ln + row * S, gv);
@@ -234,8 +269,8 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
             const int32_t ps = __ldg(d.sl_ps + k);
             const int32_t row_v = 2 * N + q;
             const int32_t row_t = 2 * N + d.n_gen + ps;
-            acc_p += __ldg(y + (row_t * S));
-            acc_q += __ldg(y + (row_v * S));
+            acc_p += src.dev_a(dv, t - rng.z);   // P_s
+            acc_q += src.dev_b(dv, t - rng.z);   // Q_g
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - __ldg(d.sl_v0 + k));
                 const double gt = 0.0 + (th_i - __ldg(d.sl_th0 + k));
@@ -279,6 +314,14 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
         }
     }
     return nrm;
+}
+
+template <int MODE, int S>
+__device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, const double* tab,
+                                                       const int32_t i, const Scen<S>& A,
+                                                       const int32_t ln, const int32_t out_l) {
+    GlobalSrc<S> src{d, A, A.y + ln, i, ln};
+    return eval_bus_src<MODE, S>(d, tab, i, src, A, ln, out_l);
 }
 
 // Batched, persistent: gridDim.x CTAs (a few per SM) stride over work items
@@ -611,7 +654,6 @@ constexpr int BATCH_W = 8;
 // alternatives on B200: 2 CTAs (more registers) and 4 CTAs (64 registers,
 // spills) were both slower.
 constexpr int BATCH_MINB = 3;
-
 template <int MODE>
 static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const double* y,
                                        const double* pq_p, const double* pq_q,

@@ -35,12 +35,22 @@
 #define PF_HD static inline
 #endif
 
-#define PF_S3 (-1.0 / 6.0)
-#define PF_S5 (1.0 / 120.0)
-#define PF_S7 (-1.0 / 5040.0)
-#define PF_C2 (-0.5)
-#define PF_C4 (1.0 / 24.0)
-#define PF_C6 (-1.0 / 720.0)
+/* polynomial coefficients; on the device they sit in the constant bank so the
+ * FP64 instructions take them as operands instead of materialising
+ * immediates every call */
+#ifdef __CUDACC__
+__device__ __constant__
+#else
+static
+#endif
+const double pf_trig_k[6] = {-1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0,
+                             -0.5, 1.0 / 24.0, -1.0 / 720.0};
+#define PF_S3 pf_trig_k[0]
+#define PF_S5 pf_trig_k[1]
+#define PF_S7 pf_trig_k[2]
+#define PF_C2 pf_trig_k[3]
+#define PF_C4 pf_trig_k[4]
+#define PF_C6 pf_trig_k[5]
 
 #ifdef __CUDACC__
 /* huge / non-finite arguments: out of line so the hot path stays small;
@@ -77,7 +87,8 @@ PF_HD void pf_sincos_tab(double x, const double* tab, double* sp, double* cp) {
      * angle difference) has k = 0, for which the reduction is the identity
      * bit for bit, so it is skipped. */
     double kf = 0.0, rh = x, rl = 0.0;
-    if (fabs(x) > 0.78539816339744828) {
+    const bool reduce = fabs(x) > 0.78539816339744828;
+    if (reduce) {
         kf = rint(x * PF_TWO_OVER_PI);
         const double ph = kf * PF_PIO2_1;
         const double pl = fma(kf, PF_PIO2_1, -ph);
@@ -116,12 +127,15 @@ PF_HD void pf_sincos_tab(double x, const double* tab, double* sp, double* cp) {
     e = (Ch - h) - Q;
     const double c = h + (e + (Cl - fma(Sh, sd, fma(Sl, dh, fma(-Ch, cm1, Ql)))));
     s = neg ? -s : s;
-    /* 4. quadrant */
-    const int q = (int)((long long)kf & 3);
-    double so = (q & 1) ? c : s;
-    double co = (q & 1) ? s : c;
-    so = (q & 2) ? -so : so;
-    co = ((q + 1) & 2) ? -co : co;
+    /* 4. quadrant (k = 0 without reduction) */
+    double so = s, co = c;
+    if (reduce) {
+        const int q = (int)((long long)kf & 3);
+        so = (q & 1) ? c : s;
+        co = (q & 1) ? s : c;
+        so = (q & 2) ? -so : so;
+        co = ((q + 1) & 2) ? -co : co;
+    }
     *sp = (x == 0.0) ? x : so; /* keep the sign of -0.0 */
     *cp = co;
 }

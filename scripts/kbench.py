@@ -19,13 +19,16 @@ t = lambda a: torch.from_numpy(a).cuda()
 dy, dp, dq, dv, do = t(y), t(pq_p), t(pq_q), t(pv_p), t(out)
 g, j, n = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K), plan.empty(K)
 _, _, by = bench.algorithmic_bytes(s, plan.nnz, K)
+mode = os.environ.get("MODE", "fj")
+gg = g if "f" in mode else None
+jj = j if "j" in mode else None
 for _ in range(3):
-    plan.eval_batched(K, dy, dp, dq, dv, do, g, j, n)
+    plan.eval_batched(K, dy, dp, dq, dv, do, gg, jj, n)
 ts = []
 for _ in range(int(os.environ.get("REPS", "20"))):
     a, b = torch.cuda.Event(True), torch.cuda.Event(True)
-    a.record(); plan.eval_batched(K, dy, dp, dq, dv, do, g, j, n); b.record()
+    a.record(); plan.eval_batched(K, dy, dp, dq, dv, do, gg, jj, n); b.record()
     torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
 med = statistics.median(ts)
-tag = os.environ.get("TAG", "")
+tag = os.environ.get("TAG", "") + f" mode={mode}"
 print(f"{tag} batched K={K}: {med:.4f} ms  {by/med/1e6:.0f} GB/s  {by/med/1e6/6552.6*100:.1f}%  evals/s {K/med*1e3:.0f}")
