@@ -39,7 +39,7 @@ __device__ __forceinline__ void pf_sincos(double x, const double* tab, double* s
 }
 
 __device__ __forceinline__ const double* stage_trig_table(double* smem) {
-    for (int t = threadIdx.x; t < PF_TRIG_N * 4; t += blockDim.x) smem[t] = pf_trig_tab[t];
+    for (int t = threadIdx.x; t < PF_TRIG_N * 4; t += blockDim.x) smem[t] = __ldg(pf_trig_tab + t);
     __syncthreads();
     return smem;
 }
@@ -107,7 +107,7 @@ __device__ __forceinline__ void stage_next_bus(const DevicePlan& d, const Scen<S
             b = A.pq_q ? A.pq_q + (int64_t)dv.y * S : nullptr;
         } else if (dv.x == DEV_PV) {
             a = A.pv_p ? A.pv_p + (int64_t)dv.y * S : nullptr;
-            b = y + (int64_t)(2 * N + __ldg(d.pv_qg + dv.y)) * S;
+            b = y + (int64_t)(2 * N + dv.y) * S;   // Q_g (pv_qg = index)
         }
         if (a) {
             prefetch_l2(a);
@@ -136,14 +136,19 @@ __device__ __forceinline__ void put_offdiag(double* __restrict__ jv, int32_t at,
 // One incidence of bus i (kernels.py:79-163 restated for one terminal):
 // adds the flow to the bus balance, the partials to the four diagonal
 // accumulators, and writes the four off-diagonal values of this neighbour.
-template <int MODE, int S>
-__device__ __forceinline__ void incidence(const double* tab, const int4 m, double4 c,
-                                          const double th_i, const double u, const double th_j,
-                                          const double w, const int32_t out_l,
-                                          double* __restrict__ jv, const int32_t rp,
-                                          const int32_t rq, const int32_t nb, double& acc_p,
-                                          double& acc_q, double& d_pt, double& d_pv,
-                                          double& d_qt, double& d_qv) {
+// The ten per-incidence quantities of one bus terminal (kernels.py:79-163
+// restated for one side): the two flows and the eight residual-row partials.
+struct IncVals {
+    double fp, fq;                 // ph / pk, qh / qk
+    double pt, pv, qt, qv;         // diagonal partials (theta_i, V_i) of rows g_p[i], g_q[i]
+    double opt, opv, oqt, oqv;     // off-diagonal partials (theta_j, V_j)
+};
+
+template <int S>
+__device__ __forceinline__ IncVals inc_vals(const double* tab, const int4 m, double4 c,
+                                            const double th_i, const double u,
+                                            const double th_j, const double w,
+                                            const int32_t out_l) {
     constexpr bool BATCH = S > 1;
     if (BATCH) {  // outaged branch in some lane's scenario: rare, so test warp-wide first
         const bool hit = m.y == out_l;
@@ -162,25 +167,48 @@ __device__ __forceinline__ void incidence(const double* tab, const int4 m, doubl
     const double t2 = c.x * si - c.y * ci;
     const double t2s = kside ? -t2 : t2;
     const double uu = u * u;                     // (-u)*u == -(u*u) exactly
-    acc_p -= uu * c.z - ab * t1;                 // ph / pk
-    acc_q -= -(uu * c.w) - ab * t2s;             // qh / qk
+    IncVals v;
+    v.fp = uu * c.z - ab * t1;                   // ph | pk
+    v.fq = -(uu * c.w) - ab * t2s;               // qh | qk
+    v.pt = -ab * t2s;                            // gph_thh | gpk_thk
+    v.pv = -(2.0 * u * c.z - w * t1);            // gph_vh  | gpk_vk
+    v.qt = ab * t1;                              // gqh_thh | gqk_thk
+    v.qv = 2.0 * u * c.w + w * t2s;              // gqh_vh  | gqk_vk
+    v.opt = ab * t2s;                            // gph_thk | gpk_thh
+    v.opv = u * t1;                              // gph_vk  | gpk_vh
+    v.oqt = -ab * t1;                            // gqh_thk | gqk_thh
+    v.oqv = u * t2s;                             // gqh_vk  | gqk_vh
+    return v;
+}
+
+// Fold one incidence into the bus's sums in list order and write its four
+// off-diagonal Jacobian values.
+template <int MODE, int S>
+__device__ __forceinline__ void inc_apply(const IncVals& v, const int4 m,
+                                          double* __restrict__ jv, const int32_t rp,
+                                          const int32_t rq, const int32_t nb, double& acc_p,
+                                          double& acc_q, double& d_pt, double& d_pv,
+                                          double& d_qt, double& d_qv) {
+    acc_p -= v.fp;
+    acc_q -= v.fq;
     if (MODE & JAC) {
-        d_pt += -ab * t2s;                       // gph_thh | gpk_thk
-        d_pv += -(2.0 * u * c.z - w * t1);       // gph_vh  | gpk_vk
-        d_qt += ab * t1;                         // gqh_thh | gqk_thk
-        d_qv += 2.0 * u * c.w + w * t2s;         // gqh_vh  | gqk_vk
+        d_pt += v.pt;
+        d_pv += v.pv;
+        d_qt += v.qt;
+        d_qv += v.qv;
         const bool first = (m.z & FIRST) != 0;
         const int32_t pos = m.z & POS_MASK;
-        put_offdiag<S>(jv, rp + pos, first, ab * t2s);        // gph_thk | gpk_thh
-        put_offdiag<S>(jv, rp + nb + pos, first, u * t1);     // gph_vk  | gpk_vh
-        put_offdiag<S>(jv, rq + pos, first, -ab * t1);        // gqh_thk | gqk_thh
-        put_offdiag<S>(jv, rq + nb + pos, first, u * t2s);    // gqh_vk  | gqk_vh
+        put_offdiag<S>(jv, rp + pos, first, v.opt);
+        put_offdiag<S>(jv, rp + nb + pos, first, v.opv);
+        put_offdiag<S>(jv, rq + pos, first, v.oqt);
+        put_offdiag<S>(jv, rq + nb + pos, first, v.oqv);
     }
 }
 
 // Operand source of the global-memory path: every read goes to HBM/L2/L1.
 template <int S>
 struct GlobalSrc {
+    static constexpr bool kPre = false;   // incidence values computed in place
     const DevicePlan& d;
     const Scen<S>& A;               // block base pointers (shared memory when batched)
     const double* __restrict__ y;   // this lane's scenario view of the state
@@ -203,14 +231,24 @@ struct GlobalSrc {
             return (S > 1 && A.pq_p) ? __ldg(A.pq_p + k * S + ln) : __ldg(d.pq_p0 + k);
         if (dv.x == DEV_PV)
             return (S > 1 && A.pv_p) ? __ldg(A.pv_p + k * S + ln) : __ldg(d.pv_p0 + k);
-        return __ldg(y + (2 * d.N + d.n_gen + __ldg(d.sl_ps + k)) * S);
+        return __ldg(y + (2 * d.N + d.n_gen + k) * S);   // P_s (sl_ps = index)
     }
     __device__ __forceinline__ double dev_b(const int4 dv, int32_t) const {
         const int32_t k = dv.y;
         if (dv.x == DEV_PQ)
             return (S > 1 && A.pq_q) ? __ldg(A.pq_q + k * S + ln) : __ldg(d.pq_q0 + k);
-        if (dv.x == DEV_PV) return __ldg(y + (2 * d.N + __ldg(d.pv_qg + k)) * S);
-        return __ldg(y + (2 * d.N + __ldg(d.sl_qg + k)) * S);
+        if (dv.x == DEV_PV) return __ldg(y + (2 * d.N + k) * S);       // Q_g (pv_qg = index)
+        return __ldg(y + (2 * d.N + d.G + k) * S);                     // Q_g (sl_qg = G + index)
+    }
+    // device constants (c, d) = PV (v0, -), Slack (v0, theta0), Shunt (g, b)
+    __device__ __forceinline__ double dev_c(const int4 dv, int32_t) const {
+        if (dv.x == DEV_PV) return __ldg(d.pv_v0 + dv.y);
+        if (dv.x == DEV_SLACK) return __ldg(d.sl_v0 + dv.y);
+        return __ldg(d.sh_g + dv.y);
+    }
+    __device__ __forceinline__ double dev_d(const int4 dv, int32_t) const {
+        if (dv.x == DEV_SLACK) return __ldg(d.sl_th0 + dv.y);
+        return __ldg(d.sh_b + dv.y);
     }
 };
 
@@ -238,10 +276,15 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
     for (int32_t e = rng.x; e < rng.y; ++e) {
         const int32_t t = e - rng.x;
         const int4 m = src.meta(e, t);
-        const double tj = src.th_j(m.x, t);
-        const double wj = src.v_j(m.x, t);
-        incidence<MODE, S>(tab, m, src.coef(e, t), th_i, v_i, tj, wj, out_l, jv, rp, rq, nb,
-                           acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
+        if constexpr (Src::kPre) {
+            inc_apply<MODE, S>(src.vals(e), m, jv, rp, rq, nb, acc_p, acc_q, d_pt, d_pv, d_qt,
+                               d_qv);
+        } else {
+            const double tj = src.th_j(m.x, t);
+            const double wj = src.v_j(m.x, t);
+            const IncVals v = inc_vals<S>(tab, m, src.coef(e, t), th_i, v_i, tj, wj, out_l);
+            inc_apply<MODE, S>(v, m, jv, rp, rq, nb, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
+        }
     }
 
     // devices in pool-segment order: PQ, PV, Slack, Shunt (residual.py:57, 91-109)
@@ -252,11 +295,11 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
             acc_p += -src.dev_a(dv, t - rng.z);
             acc_q += -src.dev_b(dv, t - rng.z);
         } else if (dv.x == DEV_PV) {
-            const int32_t row = 2 * N + __ldg(d.pv_qg + k);
+            const int32_t row = 2 * N + k;   // g_V row of the gen (pv_qg = index, plan-checked)
             acc_p += src.dev_a(dv, t - rng.z);
             acc_q += src.dev_b(dv, t - rng.z);
             if (MODE & (RES | NORM)) {
-                const double gv = 0.0 + (v_i - __ldg(d.pv_v0 + k));
+                const double gv = 0.0 + (v_i - src.dev_c(dv, t - rng.z));
                 if (MODE & RES) st_out(A.g + ln + row * S, gv);
                 nrm = max(nrm, abs_bits(gv));
             }
@@ -265,15 +308,15 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 st_out(jv + dv.w * S, 1.0);   // (g_V, V_i)
             }
         } else if (dv.x == DEV_SLACK) {
-            const int32_t q = __ldg(d.sl_qg + k);
-            const int32_t ps = __ldg(d.sl_ps + k);
+            const int32_t q = d.G + k;    // sl_qg, sl_ps are aranges (plan-checked)
+            const int32_t ps = k;
             const int32_t row_v = 2 * N + q;
             const int32_t row_t = 2 * N + d.n_gen + ps;
             acc_p += src.dev_a(dv, t - rng.z);   // P_s
             acc_q += src.dev_b(dv, t - rng.z);   // Q_g
             if (MODE & (RES | NORM)) {
-                const double gv = 0.0 + (v_i - __ldg(d.sl_v0 + k));
-                const double gt = 0.0 + (th_i - __ldg(d.sl_th0 + k));
+                const double gv = 0.0 + (v_i - src.dev_c(dv, t - rng.z));
+                const double gt = 0.0 + (th_i - src.dev_d(dv, t - rng.z));
                 if (MODE & RES) {
                     st_out(A.g + ln + row_v * S, gv);
                     st_out(A.g + ln + row_t * S, gt);
@@ -287,7 +330,7 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 st_out(jv + __ldg(d.gen_row_pos + d.n_gen + ps) * S, 1.0);    // (g_theta, theta)
             }
         } else {  // DEV_SHUNT (kernels.py:236-241, 258-262)
-            const double gsh = __ldg(d.sh_g + k), bsh = __ldg(d.sh_b + k);
+            const double gsh = src.dev_c(dv, t - rng.z), bsh = src.dev_d(dv, t - rng.z);
             const double v2 = v_i * v_i;
             acc_p += -gsh * v2;
             acc_q += bsh * v2;
@@ -405,28 +448,107 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
     if (cur >= 0) flush(cur);
 }
 
+// Single grid, one CTA per grid_buses consecutive buses (their incidences
+// are contiguous), in two phases:
+//   A: threads [B, blockDim) take one incidence each and compute its ten
+//      values into shared memory (all neighbour gathers and trig in
+//      parallel); meanwhile threads [0, B) - one per bus - load the bus
+//      header, own state and first two devices' operands;
+//   B: each bus thread folds its incidences from shared memory in list order
+//      (the reference's association), adds its devices and writes g, the
+//      Jacobian row values and the norm, with no global loads left.
+// The latency chain is ~3 dependent memory round trips per launch instead of
+// one per incidence.
+struct GridSrc : GlobalSrc<1> {
+    static constexpr bool kPre = true;
+    const IncVals* sv;
+    int32_t E0;
+    int4 h0, h1;
+    double thi, vi;
+    int4 dv0, dv1;                     // first two devices
+    double a0, b0, c0, d0, a1, b1, c1, d1;
+    __device__ __forceinline__ int4 hdr0() const { return h0; }
+    __device__ __forceinline__ int4 hdr1() const { return h1; }
+    __device__ __forceinline__ double th_i() const { return thi; }
+    __device__ __forceinline__ double v_i() const { return vi; }
+    __device__ __forceinline__ IncVals vals(int32_t e) const { return sv[e - E0]; }
+    __device__ __forceinline__ int4 dev(int32_t t, int32_t u) const {
+        return u == 0 ? dv0 : u == 1 ? dv1 : GlobalSrc<1>::dev(t, u);
+    }
+    __device__ __forceinline__ double dev_a(const int4 dv, int32_t u) const {
+        return u == 0 ? a0 : u == 1 ? a1 : GlobalSrc<1>::dev_a(dv, u);
+    }
+    __device__ __forceinline__ double dev_b(const int4 dv, int32_t u) const {
+        return u == 0 ? b0 : u == 1 ? b1 : GlobalSrc<1>::dev_b(dv, u);
+    }
+    __device__ __forceinline__ double dev_c(const int4 dv, int32_t u) const {
+        return u == 0 ? c0 : u == 1 ? c1 : GlobalSrc<1>::dev_c(dv, u);
+    }
+    __device__ __forceinline__ double dev_d(const int4 dv, int32_t u) const {
+        return u == 0 ? d0 : u == 1 ? d1 : GlobalSrc<1>::dev_d(dv, u);
+    }
+};
+
+// load device u's record and operands into registers (types it does not use
+// are left untouched: no out-of-range reads)
+__device__ __forceinline__ void grid_dev(const GlobalSrc<1>& gs, const DevicePlan& d, int32_t t,
+                                         bool have, int4& dv, double& a, double& b, double& c,
+                                         double& dd) {
+    dv = have ? __ldg(d.dev_list + t) : make_int4(-1, 0, 0, 0);
+    a = b = c = dd = 0.0;
+    if (dv.x == DEV_PQ || dv.x == DEV_PV || dv.x == DEV_SLACK) {
+        a = gs.dev_a(dv, 0);
+        b = gs.dev_b(dv, 0);
+    }
+    if (dv.x == DEV_PV || dv.x == DEV_SLACK || dv.x == DEV_SHUNT) c = gs.dev_c(dv, 0);
+    if (dv.x == DEV_SLACK || dv.x == DEV_SHUNT) dd = gs.dev_d(dv, 0);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(128) k_eval_single(const DevicePlan d,
                                                      const double* __restrict__ y,
                                                      double* __restrict__ g,
                                                      double* __restrict__ jv,
                                                      unsigned long long* __restrict__ norm) {
+    extern __shared__ __align__(16) unsigned char grid_smem[];
+    IncVals* sv = reinterpret_cast<IncVals*>(grid_smem);
     __shared__ unsigned long long red[4];
     __shared__ double s_tab[PF_TRIG_N * 4];
     const double* tab = stage_trig_table(s_tab);
-    const int32_t bus = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long nrm = 0;
-    if (bus < d.N) {
-        Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
-        nrm = eval_bus<MODE, 1>(d, tab, bus, A, 0, -1);
+    const int32_t N = d.N, B = d.grid_buses;
+    const int32_t b0 = blockIdx.x * B, b1 = min(N, b0 + B);
+    const int32_t E0 = __ldg(d.inc_ptr + b0), E1 = __ldg(d.inc_ptr + b1);
+    const int32_t i = b0 + threadIdx.x;
+    const bool own = threadIdx.x < B && i < b1;
+    Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
+    GridSrc src{{d, A, y, i, 0}, sv, E0, make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0), 0.0, 0.0};
+    if (own) {
+        src.h0 = __ldg(d.bus_row + 2 * i);
+        src.h1 = __ldg(d.bus_row + 2 * i + 1);
+        src.thi = __ldg(y + i);
+        src.vi = __ldg(y + N + i);
+        const int32_t t0 = src.h1.z, nd = src.h1.w - src.h1.z;
+        grid_dev(src, d, t0, nd > 0, src.dv0, src.a0, src.b0, src.c0, src.d0);
+        grid_dev(src, d, t0 + 1, nd > 1, src.dv1, src.a1, src.b1, src.c1, src.d1);
     }
+    const int32_t nA = blockDim.x - B;
+    for (int32_t e = E0 + (int32_t)threadIdx.x - B; threadIdx.x >= B && e < E1; e += nA) {
+        const int4 m = __ldg(d.inc_meta + e);
+        const double4 c = ldg4(d.inc_coef + e);
+        const int32_t o = m.w;
+        sv[e - E0] = inc_vals<1>(tab, m, c, __ldg(y + o), __ldg(y + N + o), __ldg(y + m.x),
+                                 __ldg(y + N + m.x), -1);
+    }
+    __syncthreads();
+    unsigned long long nrm = 0;
+    if (own) nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1);
     if (MODE & NORM) {
         for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
         __syncthreads();
         if (threadIdx.x == 0) {
-            unsigned long long m = max(max(red[0], red[1]), max(red[2], red[3]));
-            if (m) atomicMax(norm, m);
+            unsigned long long mx = max(max(red[0], red[1]), max(red[2], red[3]));
+            if (mx) atomicMax(norm, mx);
         }
     }
 }
@@ -622,7 +744,14 @@ inline unsigned grid_for(int64_t n, int threads) {
 template <int MODE>
 static void launch_single_mode(const DevicePlan& d, const double* y, double* g, double* j,
                                double* norm, cudaStream_t st) {
-    k_eval_single<MODE><<<grid_for(d.N, 128), 128, 0, st>>>(
+    const size_t smem = sizeof(IncVals) * (size_t)std::max(d.grid_max_inc, 1);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_eval_single<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = smem;
+    }
+    k_eval_single<MODE><<<grid_for(d.N, d.grid_buses), 128, smem, st>>>(
         d, y, g, j, reinterpret_cast<unsigned long long*>(norm));
 }
 

@@ -18,16 +18,21 @@ constexpr int32_t POS_MASK = (1 << 29) - 1;
 // Per-bus row descriptor (bus_row.w flag bit).
 constexpr int32_t VDIAG = 1 << 30;   // row holds a (g, V_i) diagonal entry
 
+// shared-memory bytes per incidence in the single-grid two-phase kernel
+constexpr int GRID_INC_VALS = 10;
+constexpr int GRID_INC_BYTES = 8 * GRID_INC_VALS;
+
 // Device-list entry types, in the reference's pool-segment order (residual.py:57).
 enum DevType : int32_t { DEV_PQ = 0, DEV_PV = 1, DEV_SLACK = 2, DEV_SHUNT = 3 };
 
 // Everything the evaluation kernels read.  All pointers are device memory.
 struct DevicePlan {
     int32_t N, L, P, G, S, H, n_gen, n_var, nnz, n_inc;
+    int32_t grid_buses, grid_max_inc;   // single-grid two-phase kernel partition
     // incidence lists: bus i owns [inc_ptr[i], inc_ptr[i+1]) in the order
     // (branches with h=i ascending) ++ (branches with k=i ascending)
     const int32_t* inc_ptr;   // [N+1]
-    const int4* inc_meta;     // [n_inc] {neighbour j, branch l, pos|flags, 0}
+    const int4* inc_meta;     // [n_inc] {neighbour j, branch l, pos|flags, owning bus}
     const double4* inc_coef;  // [n_inc] {g1, b1, gs, bs}: h side {gl, bl, gsh, bsh},
                               //          k side {gl2, -bl2, gsk, bsk}
     const int4* bus_row;      // [2N] bus header: [2i] = {rp, rq, nb, pos_i|VDIAG}: CSR

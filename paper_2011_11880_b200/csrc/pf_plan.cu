@@ -94,7 +94,7 @@ __global__ void k_inc_records(int32_t L, const int32_t* sorted_e, const int32_t*
     int32_t e = sorted_e[t];
     bool ks = e >= L;
     int32_t l = ks ? e - L : e;
-    meta[t] = make_int4(ks ? bh[l] : bk[l], l, ks ? KSIDE : 0, 0);
+    meta[t] = make_int4(ks ? bh[l] : bk[l], l, ks ? KSIDE : 0, ks ? bk[l] : bh[l]);
     coef[t] = ks ? make_double4(gl2[l], -bl2[l], gsk[l], bsk[l])
                  : make_double4(gl[l], bl[l], gsh[l], bsh[l]);
 }
@@ -594,6 +594,16 @@ int build(const pf_topology* t, pf_plan** out) {
     int32_t md = 0;
     for (int32_t i = 0; i < N; ++i) md = std::max(md, hptr[i + 1] - hptr[i]);
     P->max_deg = md;
+    // single-grid two-phase kernel: buses per CTA and the largest incidence
+    // count of any CTA (sizes its shared-memory staging)
+    d.grid_buses = 32;
+    for (int B : {32, 16, 8}) {
+        int32_t mx = 0;
+        for (int32_t b0 = 0; b0 < N; b0 += B) mx = std::max(mx, hptr[std::min(N, b0 + B)] - hptr[b0]);
+        d.grid_buses = B;
+        d.grid_max_inc = mx;
+        if ((int64_t)mx * GRID_INC_BYTES <= 96 * 1024) break;
+    }
     count_launch(12);
     *out = P;
     return PF_OK;
