@@ -130,6 +130,15 @@ def golden_single(name: str, raw_cols: C.RawCase, n_random: int, seed: int) -> N
         *pflow.slack_injections(s, y), *pflow.shunt_injections(s, y)])
     if s.n_var <= 400:
         out["fd_jac"] = pflow.finite_difference_jacobian(s, y)
+    # the caller of the path: pflow's own Newton solve from flat start
+    try:
+        res = pflow.newton_solve(s, pflow.flat_start(s), pflow.NewtonOptions())
+        out["newton_converged"] = np.array(res.converged)
+        out["newton_iterations"] = np.array(res.iterations)
+        out["newton_y"] = res.y
+        out["newton_mismatch"] = np.array(res.final_mismatch)
+    except pflow.SingularMatrixError:  # isolated buses: singular by construction
+        out["newton_converged"] = np.array(False)
     np.savez_compressed(OUT / f"{name}.npz", **out)
     print(f"{name}: n_var={s.n_var} nnz={jws.nnz} slots={jws.vals.size} states={len(ys)}")
 

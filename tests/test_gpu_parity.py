@@ -338,3 +338,20 @@ def test_gpu_trig_bit_identical_to_cpu_twin(tmp_path):
     assert np.array_equal(s[finite], s_ref[finite])
     assert np.array_equal(c[finite], c_ref[finite])
     assert np.array_equal(np.signbit(s[finite]), np.signbit(s_ref[finite]))
+
+
+@pytest.mark.parametrize("name", ["case2", "case5_shift", "case14", "slack_only"])
+def test_newton_driver_matches_reference_solve(name):
+    """The caller of the path (pflow/newton.py:49-112) driven by the GPU
+    evaluation: same convergence, same iteration count, same solution."""
+    from paper_2011_11880_b200.newton import NewtonOptions, newton_solve
+    from paper_2011_11880_b200.system_model import flat_start
+
+    d = load(name)
+    assert bool(d["newton_converged"])
+    s = system_of(d)
+    res = newton_solve(s, flat_start(s), NewtonOptions())
+    assert res.converged and not res.diverged
+    assert res.iterations == int(d["newton_iterations"])
+    assert res.final_mismatch <= 1e-8
+    assert np.abs(res.y - d["newton_y"]).max() < 1e-8
