@@ -38,7 +38,6 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "f+J evals/s on 70k-bus synthetic grid (fp64); HBM GB/s as % of peak"
-K_PER_RANK = 256
 
 
 def log(*a):
@@ -101,11 +100,21 @@ class Clocks:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def build_case(seed: int = 3):
+WORKLOADS = {
+    # name: (BASELINE config, scenarios per GPU, description)
+    "config3": (3, 256, "config3: 70k-bus/88k-branch grid (45k PQ, 6k PV, 1 slack), "
+                        "K=256 scenarios per GPU per step"),
+    "config4": (4, 64, "config4 stress: 200k-bus/250k-branch grid + 1% degree-50 hub buses, "
+                       "K=64 scenarios per GPU per step"),
+}
+
+
+def build_case(workload: str = "config3"):
     from paper_2011_11880_b200 import synth
     from paper_2011_11880_b200.system_model import build_system
 
-    return build_system(synth.config_case(3, seed=seed))
+    cfg = WORKLOADS[workload][0]
+    return build_system(synth.config_case(cfg, seed=cfg))
 
 
 def blocked_inputs(sys_, K, seed):
@@ -161,20 +170,21 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    sys_ = build_case()
+    sys_ = build_case(args.workload)
+    K = WORKLOADS[args.workload][1]
     threads = os.cpu_count() or 1
-    r = cpu_reference(sys_, K_PER_RANK, 1000, args.steps, args.warmup, threads)
+    r = cpu_reference(sys_, K, 1000, args.steps, args.warmup, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "evals/s",
         "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config3: 70k-bus/88k-branch grid, K=256 scenarios per step "
-                               "(load/PV scaling + 1 outage each), f+J per scenario",
+        "config": {"workload": WORKLOADS[args.workload][2] + " (load/PV scaling + 1 outage "
+                               "each), f+J per scenario",
                    "parallelism": f"{threads} host threads, one scenario per thread at a time"},
         "cpu_baseline": {"value": r["value"], "unit": "evals/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{r['steps']} steps x {K_PER_RANK} scenarios, pflow wf{r['wf']} "
+                         "sample": f"{r['steps']} steps x {K} scenarios, pflow wf{r['wf']} "
                                    "restated in C (oracle/), workspace outputs"},
         "e2e": {"value": r["value"], "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -201,8 +211,8 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    K = K_PER_RANK
-    sys_ = build_case()
+    K = WORKLOADS[args.workload][1]
+    sys_ = build_case(args.workload)
     plan = Plan(sys_, device=dev)
     per_scen, static, bytes_launch = algorithmic_bytes(sys_, plan.nnz, K)
     y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K, seed=1000 + rank)
@@ -293,13 +303,14 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {
-                "workload": "config3: 70k-bus/88k-branch grid (45k PQ, 6k PV, 1 slack), "
-                            f"K={K} scenarios per GPU per step, per-device load U(0.8,1.2) + "
+                "workload": WORKLOADS[args.workload][2] + ", per-device load U(0.8,1.2) + "
                             "PV U(0.5,1.5) scaling, 1 outaged branch each; fused f+J+inf-norm",
                 "n_var": plan.n_var, "nnz": plan.nnz, "scenarios_per_gpu": K,
                 "parallelism": f"scenario-sharded x{world}" + (", NCCL all-gather of norms"
                                                                if world > 1 else ""),
-                "l2": "inputs+outputs per step 2.8 GB > 126 MB L2 (no flush needed)",
+                "l2": f"inputs+outputs per step {bytes_launch / 1e9:.2f} GB > 126 MB L2 "
+                      "(no flush needed)",
+                "max_bus_degree": plan.max_degree,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
@@ -316,14 +327,14 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
 
-    if rank == 0 and world == 1 and not args.no_single:
+    if rank == 0 and world == 1 and not args.no_single and args.workload == "config3":
         line["single_grid"] = single_grid(dev, steps=max(20, args.steps))
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         r = cpu_reference(sys_, K, 2000, 1, 1, threads, min_seconds=args.cpu_seconds)
         line["cpu_baseline"] = {
             "value": r["value"], "unit": "evals/s", "cores": threads, "kind": "port",
-            "sample": f"{r['steps']} x {K} config-3 scenarios, pflow wf{r['wf']} restated in C "
+            "sample": f"{r['steps']} x {K} {args.workload} scenarios, pflow wf{r['wf']} restated in C "
                       "(oracle/), one scenario per thread, workspace outputs"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -406,6 +417,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-single", action="store_true", help="skip the single-grid leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

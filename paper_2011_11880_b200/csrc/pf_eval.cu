@@ -429,13 +429,20 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
             out_l = (outage && s < K) ? __ldg(outage + s) : -1;
             __syncthreads();
         }
-        const int32_t bus = grp * W + warp;
+        // processing order: high-degree buses first, so they do not form a
+        // straggler tail at the end of each block's sweep
+        const int32_t slot = grp * W + warp;
+        const int32_t bus = slot < d.N ? __ldg(d.bus_order + slot) : d.N;
         // stage the next item of this warp (same block only) behind this one
         const int32_t gn = grp + gridDim.x;
-        const int32_t bn = gn * W + warp;
-        const bool pre = gn < n_groups && bn < d.N;
+        const int32_t sn = gn * W + warp;
+        const bool pre = gn < n_groups && sn < d.N;
+        int32_t bn = 0;
         int4 rng_n = make_int4(0, 0, 0, 0);
-        if (pre) rng_n = __ldg(d.bus_row + 2 * bn + 1);
+        if (pre) {
+            bn = __ldg(d.bus_order + sn);
+            rng_n = __ldg(d.bus_row + 2 * bn + 1);
+        }
         if (bus < d.N && blk * PF_LANES + lane < K)
             nrm = max(nrm, eval_bus<MODE, PF_LANES>(d, tab, bus, A, lane, out_l));
         if (pre) stage_next_bus<PF_LANES>(d, A, bn, rng_n, lane);

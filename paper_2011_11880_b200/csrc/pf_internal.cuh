@@ -18,6 +18,9 @@ constexpr int32_t POS_MASK = (1 << 29) - 1;
 // Per-bus row descriptor (bus_row.w flag bit).
 constexpr int32_t VDIAG = 1 << 30;   // row holds a (g, V_i) diagonal entry
 
+// buses with at least this many incidences are scheduled first (batched)
+constexpr int HUB_DEG = 16;
+
 // shared-memory bytes per incidence in the single-grid two-phase kernel
 constexpr int GRID_INC_VALS = 10;
 constexpr int GRID_INC_BYTES = 8 * GRID_INC_VALS;
@@ -39,6 +42,7 @@ struct DevicePlan {
                               // offsets of rows g_p[i], g_q[i], theta-block size,
                               // diagonal rank; [2i+1] = {e0, e1, t0, t1}: incidence
                               // and device-list ranges (one 32-byte load)
+    const int32_t* bus_order; // [N] batched processing order: degree >= HUB_DEG first
     const int32_t* dev_ptr;   // [N+1]
     const int4* dev_list;     // [n_dev] {type, index, jpos_a, jpos_b}
     // device parameters (base values; scenarios may override P/Q)

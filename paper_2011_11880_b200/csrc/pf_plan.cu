@@ -594,6 +594,21 @@ int build(const pf_topology* t, pf_plan** out) {
     int32_t md = 0;
     for (int32_t i = 0; i < N; ++i) md = std::max(md, hptr[i + 1] - hptr[i]);
     P->max_deg = md;
+    // batched processing order: high-degree buses first, then the rest, each
+    // in bus order (the identity when there are no hubs)
+    {
+        std::vector<int32_t> order;
+        order.reserve(N);
+        for (int32_t i = 0; i < N; ++i)
+            if (hptr[i + 1] - hptr[i] >= HUB_DEG) order.push_back(i);
+        for (int32_t i = 0; i < N; ++i)
+            if (hptr[i + 1] - hptr[i] < HUB_DEG) order.push_back(i);
+        int32_t* bus_order;
+        PF_TRY(owned_alloc(P, &bus_order, N));
+        PF_TRY(cudaMemcpy(bus_order, order.data(), sizeof(int32_t) * (size_t)N,
+                          cudaMemcpyHostToDevice));
+        d.bus_order = bus_order;
+    }
     // single-grid two-phase kernel: buses per CTA and the largest incidence
     // count of any CTA (sizes its shared-memory staging)
     d.grid_buses = 32;

@@ -355,3 +355,37 @@ def test_newton_driver_matches_reference_solve(name):
     assert res.iterations == int(d["newton_iterations"])
     assert res.final_mismatch <= 1e-8
     assert np.abs(res.y - d["newton_y"]).max() < 1e-8
+
+
+def test_config4_full_size_sampled_scenarios():
+    """BASELINE config 4 at full size (200k buses, 250k branches + degree-50
+    hubs): 32 scenarios on the GPU, four of them checked against the oracle."""
+    from paper_2011_11880_b200.batched import ScenarioBuffers
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    s = build_system(synth.config_case(4, seed=4))
+    plan = _plan(s)
+    assert plan.max_degree >= 50
+    K = 32
+    sb = synth.make_scenarios(s, K, seed=9)
+    buf = ScenarioBuffers(plan, K)
+    buf.upload(sb)
+    buf.evaluate()
+    torch.cuda.synchronize()
+    o = oracle.Oracle(s)
+    _, _, perm = plan.pattern_csc()
+    cptr, cidx = o.pattern_csc()
+    pptr, pidx, _ = plan.pattern_csc()
+    assert np.array_equal(cptr, pptr) and np.array_equal(cidx, pidx)
+    pick = [0, 7, 19, 31]
+    g_ref, j_ref, n_ref = o.eval_scenarios(
+        len(pick), to_blocked(sb.y[:, pick].T), to_blocked(sb.pq_p[:, pick].T),
+        to_blocked(sb.pq_q[:, pick].T), to_blocked(sb.pv_p[:, pick].T), sb.outage[pick],
+        nthreads=8)
+    g_ref = from_blocked(g_ref, len(pick), plan.n_var)
+    j_ref = from_blocked(j_ref, len(pick), plan.nnz)
+    G = buf.residual()
+    J = buf.jacobian_csr()
+    for i, k in enumerate(pick):
+        assert_parity(G[k], g_ref[i], f"config4 scenario {k} g")
+        assert_parity(J[k][perm], j_ref[i], f"config4 scenario {k} J")
