@@ -389,3 +389,46 @@ def test_config4_full_size_sampled_scenarios():
     for i, k in enumerate(pick):
         assert_parity(G[k], g_ref[i], f"config4 scenario {k} g")
         assert_parity(J[k][perm], j_ref[i], f"config4 scenario {k} J")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_grids_fuzz(seed):
+    """Randomised small grids (parallel and reversed branches, shifts, taps,
+    shunts, out-of-service rows, hubs, isolated buses): pattern bit-exact and
+    values within tolerance against the oracle, single grid and batched."""
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    rng = np.random.default_rng(1000 + seed)
+    nb = int(rng.integers(2, 400))
+    nbr = int(rng.integers(nb - 1, 2 * nb + 3))
+    case = synth.synth_case(nb, nbr, seed=seed, pq_frac=float(rng.uniform(0, 1)),
+                            pv_frac=float(rng.uniform(0, 0.5)),
+                            shunt_frac=float(rng.uniform(0, 0.5)),
+                            shift_frac=float(rng.uniform(0, 0.5)),
+                            out_of_service_frac=float(rng.uniform(0, 0.2)),
+                            hub_frac=0.05 if nb > 60 else 0.0, hub_degree=20)
+    s = build_system(case)
+    plan = _plan(s)
+    o = oracle.Oracle(s)
+    cptr, cidx = o.pattern_csc()
+    pptr, pidx, perm = plan.pattern_csc()
+    assert np.array_equal(cptr, pptr) and np.array_equal(cidx, pidx)
+    y = random_state(s, seed)
+    g, j, _ = _eval(plan, y)
+    assert_parity(g, o.residual(y), "g")
+    assert_parity(j[perm], o.jacobian(y), "J")
+    K = int(rng.integers(1, 70))
+    sb = synth.make_scenarios(s, K, seed=seed)
+    t = lambda a: _dev(to_blocked(a))
+    gb, jb, nr = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K), plan.empty(K)
+    outage = torch.as_tensor(sb.outage, device="cuda")
+    plan.eval_batched(K, t(sb.y.T), t(sb.pq_p.T), t(sb.pq_q.T), t(sb.pv_p.T), outage, gb, jb, nr)
+    torch.cuda.synchronize()
+    gr, jr, nrr = o.eval_scenarios(K, to_blocked(sb.y.T), to_blocked(sb.pq_p.T),
+                                   to_blocked(sb.pq_q.T), to_blocked(sb.pv_p.T), sb.outage,
+                                   nthreads=4)
+    G = from_blocked(gb.cpu().numpy(), K, plan.n_var)
+    J = from_blocked(jb.cpu().numpy(), K, plan.nnz)
+    assert_parity(G, from_blocked(gr, K, plan.n_var), "batched g")
+    assert_parity(J[:, perm], from_blocked(jr, K, plan.nnz), "batched J")
+    assert np.array_equal(nr[:K].cpu().numpy(), np.abs(G).max(axis=1))
