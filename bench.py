@@ -265,6 +265,10 @@ def run_gpu(args):
     value = world * K * args.steps / (ms_total / 1e3)
     peak, peak_kind = peaks()
     achieved = bytes_launch / (kern_avg / 1e3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():  # measured by ncu on this kernel (see that file's note)
+        traffic = json.loads(tfile.read_text()).get(args.workload, {}).get("bytes")
 
     # norms sanity (device-resident result used by Newton callers)
     assert torch.isfinite(d_n[:K]).all()
@@ -313,7 +317,7 @@ def run_gpu(args):
                 "max_bus_degree": plan.max_degree,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "bytes_per_scenario": per_scen, "static_bytes": static,
