@@ -550,12 +550,30 @@ __global__ void __launch_bounds__(128) k_eval_single(const DevicePlan d,
     unsigned long long nrm = 0;
     if (own) nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1);
     if (MODE & NORM) {
+        // per-CTA max into the plan's scratch; the last CTA to finish reduces
+        // them and re-arms the counter, so no separate zeroing launch is needed
         for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
         __syncthreads();
+        __shared__ bool last;
         if (threadIdx.x == 0) {
-            unsigned long long mx = max(max(red[0], red[1]), max(red[2], red[3]));
-            if (mx) atomicMax(norm, mx);
+            d.norm_part[blockIdx.x] = max(max(red[0], red[1]), max(red[2], red[3]));
+            __threadfence();
+            last = atomicAdd(d.norm_count, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            unsigned long long mx = 0;
+            for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+                mx = max(mx, __ldcg(d.norm_part + b));
+            for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                *norm = max(max(red[0], red[1]), max(red[2], red[3]));
+                *d.norm_count = 0;
+            }
         }
     }
 }
@@ -764,11 +782,10 @@ static void launch_single_mode(const DevicePlan& d, const double* y, double* g, 
 
 cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, double* j,
                                double* norm, cudaStream_t st) {
-    if (norm) {
-        cudaError_t e = cudaMemsetAsync(norm, 0, sizeof(double), st);
-        if (e != cudaSuccess) return e;
+    if (d.N == 0) {
+        if (norm) return cudaMemsetAsync(norm, 0, sizeof(double), st);
+        return cudaSuccess;
     }
-    if (d.N == 0) return cudaSuccess;
     const int mode = (g ? RES : 0) | (j ? JAC : 0) | (norm ? NORM : 0);
     switch (mode) {
         case RES: launch_single_mode<RES>(d, y, g, j, norm, st); break;

@@ -32,6 +32,9 @@ enum DevType : int32_t { DEV_PQ = 0, DEV_PV = 1, DEV_SLACK = 2, DEV_SHUNT = 3 };
 struct DevicePlan {
     int32_t N, L, P, G, S, H, n_gen, n_var, nnz, n_inc;
     int32_t grid_buses, grid_max_inc;   // single-grid two-phase kernel partition
+    // single-grid norm: per-CTA maxima and a completion counter (last CTA reduces)
+    unsigned long long* norm_part;      // [grid_for(N, grid_buses)]
+    unsigned int* norm_count;           // 0 between launches
     // incidence lists: bus i owns [inc_ptr[i], inc_ptr[i+1]) in the order
     // (branches with h=i ascending) ++ (branches with k=i ascending)
     const int32_t* inc_ptr;   // [N+1]

@@ -603,6 +603,8 @@ int build(const pf_topology* t, pf_plan** out) {
             if (hptr[i + 1] - hptr[i] >= HUB_DEG) order.push_back(i);
         for (int32_t i = 0; i < N; ++i)
             if (hptr[i + 1] - hptr[i] < HUB_DEG) order.push_back(i);
+        // (kept as a load even when it is the identity: measured faster on
+        // B200 than a conditional bypass, 0.738 vs 0.776 ms at config 3)
         int32_t* bus_order;
         PF_TRY(owned_alloc(P, &bus_order, N));
         PF_TRY(cudaMemcpy(bus_order, order.data(), sizeof(int32_t) * (size_t)N,
@@ -618,6 +620,16 @@ int build(const pf_topology* t, pf_plan** out) {
         d.grid_buses = B;
         d.grid_max_inc = mx;
         if ((int64_t)mx * GRID_INC_BYTES <= 96 * 1024) break;
+    }
+    // single-grid norm scratch (the counter must start at zero)
+    {
+        unsigned long long* part;
+        unsigned int* cnt;
+        PF_TRY(owned_alloc(P, &part, (N + d.grid_buses - 1) / d.grid_buses + 1));
+        PF_TRY(owned_alloc(P, &cnt, 1));
+        PF_TRY(cudaMemset(cnt, 0, sizeof(unsigned int)));
+        d.norm_part = part;
+        d.norm_count = cnt;
     }
     count_launch(12);
     *out = P;

@@ -28,7 +28,7 @@
 #include "pf_trig_table.h"
 
 #ifdef __CUDACC__
-#define PF_HD __host__ __device__ __forceinline__
+#define PF_HD __device__ __forceinline__
 #else
 #include <math.h>
 #include <stdbool.h>
