@@ -13,7 +13,8 @@ include/pfgpu.h).  Modules that need the GPU import torch lazily, so the
 host model layer works on CPU-only machines.
 """
 
-from .case import RawCase, Violation, from_rows, make_case, validate_case
+from .case import (CaseFormatError, RawCase, Violation, from_rows, make_case, parse_case,
+                   parse_case_file, validate_case, write_case)
 from .system_model import (AddressMap, LineGroup, PowerSystem, PqGroup, PvGroup, ShuntGroup,
                            SlackGroup, build_system, count_variables, flat_start, random_state)
 
@@ -44,7 +45,7 @@ def __getattr__(name):
 
 
 __all__ = [
-    "AddressMap", "JacobianWorkspace", "LineGroup", "Plan", "PowerSystem", "PqGroup",
+    "CaseFormatError", "parse_case", "parse_case_file", "write_case", "AddressMap", "JacobianWorkspace", "LineGroup", "Plan", "PowerSystem", "PqGroup",
     "PvGroup", "RawCase", "ResidualWorkspace", "ScenarioBuffers", "ShuntGroup", "SlackGroup",
     "Violation", "build_system", "count_variables", "evaluate_jacobian", "evaluate_residual",
     "finite_difference_jacobian", "flat_start", "from_rows", "gather_norms", "make_case",

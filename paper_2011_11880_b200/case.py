@@ -2,9 +2,10 @@
 
 Mirrors the reference's ``RawCase`` (pflow/case_io.py:24-68) field for field,
 but stores each MATPOWER column as one numpy array instead of a list of row
-records, so 200k-bus synthetic grids build in milliseconds.  MATPOWER text
-parsing is out of scope for this engine; the reference's
-own ``RawCase`` objects are accepted through :func:`from_rows`.
+records, so 200k-bus synthetic grids build in milliseconds.  The reference's
+own ``RawCase`` objects are accepted through :func:`from_rows`;
+``parse_case``/``parse_case_file``/``write_case`` read and write the MATPOWER
+numeric subset directly.
 
 ``validate_case`` restates pflow/case_io.py:189-232 (same violation codes and
 row indices) vectorised.
@@ -195,3 +196,147 @@ def validate_case(raw: RawCase) -> list[Violation]:
         if zero_z[i]:
             out.append(Violation("ZERO_IMPEDANCE", i, f"in-service branch {i} has r = x = 0"))
     return out
+
+
+# ---------------------------------------------------------------------------
+# MATPOWER case text (on-disk input)
+# ---------------------------------------------------------------------------
+
+class CaseFormatError(ValueError):
+    """Malformed case text; ``line`` is 1-based when known (pflow/case_io.py:16-21)."""
+
+    def __init__(self, message: str, line: int = 0):
+        super().__init__(f"line {line}: {message}" if line else message)
+        self.line = line
+
+
+# minimum columns consumed per MATPOWER v2 matrix
+_MIN_COLS = {"bus": 10, "gen": 8, "branch": 11}
+
+
+def parse_case(text: str, name: str = "") -> RawCase:
+    """Parse the numeric-matrix subset of MATPOWER v2 case text.
+
+    Accepts ``baseMVA`` and the ``bus``/``gen``/``branch`` assignments
+    (``mpc.`` prefix optional), ``%`` comments, rows ended by ``;`` or a
+    newline.  Errors match pflow/case_io.py:85-158: malformed matrix,
+    non-numeric token, too few columns, missing baseMVA or matrix, matrix
+    assigned twice, duplicate bus id - each with its line number.  A tap
+    ratio of 0 becomes 1.0 (MATPOWER convention).
+    """
+    base_mva = None
+    rows: dict[str, list[list[float]]] = {}
+    lines_of: dict[str, list[int]] = {}
+    current = None
+    lines = text.splitlines()
+    for lineno, raw in enumerate(lines, start=1):
+        body = raw.split("%", 1)[0].strip()
+        if not body:
+            continue
+        if current is None:
+            lhs, eq, rhs = body.partition("=")
+            if not eq:
+                continue
+            key = lhs.strip().split(".")[-1]
+            rhs = rhs.strip()
+            if key == "baseMVA":
+                try:
+                    base_mva = float(rhs.rstrip(";").strip())
+                except ValueError:
+                    raise CaseFormatError(f"baseMVA is not numeric: {rhs!r}", lineno) from None
+                continue
+            if key not in _MIN_COLS:
+                continue
+            if not rhs.startswith("["):
+                raise CaseFormatError(f"expected '[' to open matrix {key!r}", lineno)
+            if key in rows:
+                raise CaseFormatError(f"matrix {key!r} assigned twice", lineno)
+            rows[key], lines_of[key], current = [], [], key
+            body = rhs[1:]
+        closed = "]" in body
+        for seg in body.split("]", 1)[0].split(";"):
+            toks = seg.split()
+            if not toks:
+                continue
+            if len(toks) < _MIN_COLS[current]:
+                raise CaseFormatError(f"matrix {current!r} row has {len(toks)} columns, "
+                                      f"needs at least {_MIN_COLS[current]}", lineno)
+            try:
+                rows[current].append([float(t) for t in toks])
+            except ValueError:
+                bad = next(t for t in toks if not _is_float(t))
+                raise CaseFormatError(f"non-numeric token {bad!r} in matrix {current!r}",
+                                      lineno) from None
+            lines_of[current].append(lineno)
+        if closed:
+            current = None
+    if current is not None:
+        raise CaseFormatError(f"matrix {current!r} is never closed with '];'", len(lines))
+    if base_mva is None:
+        raise CaseFormatError("missing required scalar 'baseMVA'")
+    for key in ("bus", "gen", "branch"):
+        if key not in rows:
+            raise CaseFormatError(f"missing required matrix '{key}'")
+    seen: set[int] = set()
+    for r, ln in zip(rows["bus"], lines_of["bus"]):
+        bid = int(r[0])
+        if bid in seen:
+            raise CaseFormatError(f"duplicate bus id {bid}", ln)
+        seen.add(bid)
+
+    def col(key, j):
+        return np.array([r[j] for r in rows[key]], dtype=np.float64)
+
+    bus = {"bus_id": col("bus", 0).astype(np.int64), "bus_type": col("bus", 1).astype(np.int64),
+           "pd": col("bus", 2), "qd": col("bus", 3), "gs": col("bus", 4), "bs": col("bus", 5),
+           "vm": col("bus", 7), "va": col("bus", 8), "base_kv": col("bus", 9)}
+    gen = {"gen_bus": col("gen", 0).astype(np.int64), "pg": col("gen", 1), "qg": col("gen", 2),
+           "qmax": col("gen", 3), "qmin": col("gen", 4), "vg": col("gen", 5),
+           "gen_status": col("gen", 7).astype(np.int64)}
+    ratio = col("branch", 8)
+    branch = {"from_bus": col("branch", 0).astype(np.int64),
+              "to_bus": col("branch", 1).astype(np.int64), "r": col("branch", 2),
+              "x": col("branch", 3), "b": col("branch", 4),
+              "ratio": np.where(ratio != 0.0, ratio, 1.0), "angle": col("branch", 9),
+              "br_status": col("branch", 10).astype(np.int64)}
+    return make_case(base_mva, bus, gen, branch, name=name)
+
+
+def _is_float(tok: str) -> bool:
+    try:
+        float(tok)
+        return True
+    except ValueError:
+        return False
+
+
+def parse_case_file(path) -> RawCase:
+    """Read and parse a MATPOWER case file (UTF-8); the case is named after the file."""
+    from pathlib import Path
+
+    p = Path(path)
+    return parse_case(p.read_text(encoding="utf-8"), name=p.stem)
+
+
+def write_case(case: RawCase) -> str:
+    """Case text that :func:`parse_case` reads back bit-identically (%.17g);
+    unconsumed MATPOWER columns are written as neutral placeholders."""
+    g = lambda v: format(float(v), ".17g")
+    out = [f"function mpc = {case.name or 'case'}", "mpc.version = '2';",
+           f"mpc.baseMVA = {g(case.base_mva)};", "mpc.bus = ["]
+    for i in range(case.n_bus):
+        out.append(f"\t{int(case.bus_id[i])}\t{int(case.bus_type[i])}\t{g(case.pd[i])}"
+                   f"\t{g(case.qd[i])}\t{g(case.gs[i])}\t{g(case.bs[i])}\t1\t{g(case.vm[i])}"
+                   f"\t{g(case.va[i])}\t{g(case.base_kv[i])}\t1\t1.1\t0.9;")
+    out += ["];", "mpc.gen = ["]
+    for i in range(case.n_gen):
+        out.append(f"\t{int(case.gen_bus[i])}\t{g(case.pg[i])}\t{g(case.qg[i])}"
+                   f"\t{g(case.qmax[i])}\t{g(case.qmin[i])}\t{g(case.vg[i])}\t100"
+                   f"\t{int(case.gen_status[i])}\t0\t0;")
+    out += ["];", "mpc.branch = ["]
+    for i in range(case.n_branch):
+        out.append(f"\t{int(case.from_bus[i])}\t{int(case.to_bus[i])}\t{g(case.r[i])}"
+                   f"\t{g(case.x[i])}\t{g(case.b[i])}\t0\t0\t0\t{g(case.ratio[i])}"
+                   f"\t{g(case.angle[i])}\t{int(case.br_status[i])}\t-360\t360;")
+    out.append("];")
+    return "\n".join(out) + "\n"
