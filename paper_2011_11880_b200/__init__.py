@@ -37,6 +37,10 @@ def __getattr__(name):
         from . import jacobian
 
         return getattr(jacobian, name)
+    if name in ("NewtonOptions", "SolveResult", "newton_solve"):
+        from . import newton
+
+        return getattr(newton, name)
     if name in ("ScenarioBuffers", "gather_norms", "shard"):
         from . import batched
 
@@ -45,9 +49,10 @@ def __getattr__(name):
 
 
 __all__ = [
-    "CaseFormatError", "parse_case", "parse_case_file", "write_case", "AddressMap", "JacobianWorkspace", "LineGroup", "Plan", "PowerSystem", "PqGroup",
-    "PvGroup", "RawCase", "ResidualWorkspace", "ScenarioBuffers", "ShuntGroup", "SlackGroup",
-    "Violation", "build_system", "count_variables", "evaluate_jacobian", "evaluate_residual",
-    "finite_difference_jacobian", "flat_start", "from_rows", "gather_norms", "make_case",
-    "random_state", "shard", "symbolic_pattern", "validate_case",
+    "AddressMap", "CaseFormatError", "JacobianWorkspace", "LineGroup", "NewtonOptions", "Plan",
+    "PowerSystem", "PqGroup", "PvGroup", "RawCase", "ResidualWorkspace", "ScenarioBuffers",
+    "ShuntGroup", "SlackGroup", "SolveResult", "Violation", "build_system", "count_variables",
+    "evaluate_jacobian", "evaluate_residual", "finite_difference_jacobian", "flat_start",
+    "from_rows", "gather_norms", "make_case", "newton_solve", "parse_case", "parse_case_file",
+    "random_state", "shard", "symbolic_pattern", "validate_case", "write_case",
 ]
