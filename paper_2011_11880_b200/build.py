@@ -35,10 +35,26 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def build_variant(name: str, defines: list[str]) -> Path:
+    """Dev tool: build/var/<name>.so with extra -D flags (A/B kernel timing)."""
+    out_dir = BUILD / "var"
+    out_dir.mkdir(parents=True, exist_ok=True)
+    objs = []
+    for src, extra in UNITS.items():
+        o = out_dir / f"{name}.{src}.o"
+        subprocess.run([nvcc(), *COMMON, *extra, *[f"-D{d}" for d in defines], "-c",
+                        str(CSRC / src), "-o", str(o)], check=True)
+        objs.append(o)
+    lib = out_dir / f"{name}.so"
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-cudart",
+                    "static"], check=True)
+    return lib
+
+
 def build(verbose: bool = False, force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
     objs = []
-    deps = [CSRC / "pf_internal.cuh", ROOT / "include" / "pfgpu.h"]
+    deps = [*CSRC.glob("*.h"), *CSRC.glob("*.cuh"), ROOT / "include" / "pfgpu.h"]
     for src, extra in UNITS.items():
         s = CSRC / src
         o = BUILD / (src + ".o")
@@ -58,5 +74,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
-    print(OUT)
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":   # --variant NAME [DEFINE ...]
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        build(verbose="-v" in sys.argv, force="-f" in sys.argv)
+        print(OUT)

@@ -10,9 +10,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 from paper_2011_11880_b200.plan import Plan  # noqa: E402
 
-K = int(os.environ.get("K", "256"))
-cfg_seed = 3
-s = bench.build_case()
+WL = os.environ.get("WORKLOAD", "config3")
+K = int(os.environ.get("K", str(bench.WORKLOADS[WL][1])))
+s = bench.build_case(WL)
 plan = Plan(s)
 y, pq_p, pq_q, pv_p, out = bench.blocked_inputs(s, K, 1000)
 t = lambda a: torch.from_numpy(a).cuda()
