@@ -144,25 +144,14 @@ struct IncVals {
     double opt, opv, oqt, oqv;     // off-diagonal partials (theta_j, V_j)
 };
 
-template <int S>
-__device__ __forceinline__ IncVals inc_vals(const double* tab, const int4 m, double4 c,
-                                            const double th_i, const double u,
-                                            const double th_j, const double w,
-                                            const int32_t out_l) {
-    constexpr bool BATCH = S > 1;
-    if (BATCH) {  // outaged branch in some lane's scenario: rare, so test warp-wide first
-        const bool hit = m.y == out_l;
-        if (__any_sync(__activemask(), hit) && hit) c = make_double4(0.0, 0.0, 0.0, 0.0);
-    }
-    const bool kside = (m.z & KSIDE) != 0;
-    // thk = theta_h - theta_k (kernels.py:86)
-    const double thk = kside ? (th_j - th_i) : (th_i - th_j);
-    double si, ci;
-    pf_sincos(thk, tab, &si, &ci);
+// The ten values of one terminal from sin/cos of thk = theta_h - theta_k
+// (kernels.py:86-88), the terminal's coefficients c and u = V_i, w = V_j.
+// h side: c = {gl, bl, gsh, bsh}.  k side: c = {gl2, -bl2, gsk, bsk}, so
+// t1 = gl2 ci - bl2 si = t1k and t2 = gl2 si + bl2 ci = t2k, with t2s = -t2k.
+// Sign flips are exact, so every term is bit-identical to kernels.py:90-163.
+__device__ __forceinline__ IncVals inc_terms(const bool kside, const double si, const double ci,
+                                             const double4 c, const double u, const double w) {
     const double ab = u * w;
-    // h side: t1h = gl ci + bl si, t2h = gl si - bl ci.  k side with
-    // b1 = -bl2: t1k = gl2 ci - bl2 si, and t2s = -t2k.  Sign flips are
-    // exact, so every term is bit-identical to kernels.py:90-163.
     const double t1 = c.x * ci + c.y * si;
     const double t2 = c.x * si - c.y * ci;
     const double t2s = kside ? -t2 : t2;
@@ -181,14 +170,30 @@ __device__ __forceinline__ IncVals inc_vals(const double* tab, const int4 m, dou
     return v;
 }
 
-// Fold one incidence into the bus's sums in list order and write its four
-// off-diagonal Jacobian values.
-template <int MODE, int S>
-__device__ __forceinline__ void inc_apply(const IncVals& v, const int4 m,
-                                          double* __restrict__ jv, const int32_t rp,
-                                          const int32_t rq, const int32_t nb, double& acc_p,
-                                          double& acc_q, double& d_pt, double& d_pv,
-                                          double& d_qt, double& d_qv) {
+// One incidence of bus i against neighbour j (theta_i, u = V_i, theta_j, w = V_j).
+template <int S>
+__device__ __forceinline__ IncVals inc_vals(const double* tab, const int4 m, double4 c,
+                                            const double th_i, const double u,
+                                            const double th_j, const double w,
+                                            const int32_t out_l) {
+    constexpr bool BATCH = S > 1;
+    if (BATCH) {  // outaged branch in some lane's scenario: rare, so test warp-wide first
+        const bool hit = m.y == out_l;
+        if (__any_sync(__activemask(), hit) && hit) c = make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+    const bool kside = (m.z & KSIDE) != 0;
+    // thk = theta_h - theta_k (kernels.py:86)
+    const double thk = kside ? (th_j - th_i) : (th_i - th_j);
+    double si, ci;
+    pf_sincos(thk, tab, &si, &ci);
+    return inc_terms(kside, si, ci, c, u, w);
+}
+
+// Fold one incidence into the bus's sums, in list order.
+template <int MODE>
+__device__ __forceinline__ void inc_fold(const IncVals& v, double& acc_p, double& acc_q,
+                                         double& d_pt, double& d_pv, double& d_qt,
+                                         double& d_qv) {
     acc_p -= v.fp;
     acc_q -= v.fq;
     if (MODE & JAC) {
@@ -196,24 +201,63 @@ __device__ __forceinline__ void inc_apply(const IncVals& v, const int4 m,
         d_pv += v.pv;
         d_qt += v.qt;
         d_qv += v.qv;
-        const bool first = (m.z & FIRST) != 0;
-        const int32_t pos = m.z & POS_MASK;
-        put_offdiag<S>(jv, rp + pos, first, v.opt);
-        put_offdiag<S>(jv, rp + nb + pos, first, v.opv);
-        put_offdiag<S>(jv, rq + pos, first, v.oqt);
-        put_offdiag<S>(jv, rq + nb + pos, first, v.oqv);
     }
 }
 
-// Sources whose incidence values were computed beforehand (single-grid phase
-// A) set kPre; the others compute them in place.
+// Jacobian writers.  GlobalJ stores straight to the value array (batched:
+// lane stride S); StagedJ (single grid) keeps the rows g_p, g_q of the CTA's
+// buses in shared memory and writes other rows (g_V, g_theta) through.
+template <int S>
+struct GlobalJ {
+    double* __restrict__ jv;
+    __device__ __forceinline__ void put(int32_t at, double v) const { st_out(jv + at * S, v); }
+    // reference assembly: acc = 0.0; acc += slot ... (kernels.py:277-282)
+    __device__ __forceinline__ void add(int32_t at, bool first, double v) const {
+        put_offdiag<S>(jv, at, first, v);
+    }
+};
+
+struct StagedJ {
+    double* jst;                  // [p1 - p0] rows g_p, then [q1 - q0] rows g_q
+    double* __restrict__ jv;
+    int32_t p0, p1, q0, q1;
+    __device__ __forceinline__ double* loc(int32_t at) const {
+        if (at >= p0 && at < p1) return jst + (at - p0);
+        if (at >= q0 && at < q1) return jst + (p1 - p0) + (at - q0);
+        return nullptr;
+    }
+    __device__ __forceinline__ void put(int32_t at, double v) const {
+        double* p = loc(at);
+        if (p) *p = v;
+        else jv[at] = v;
+    }
+    __device__ __forceinline__ void add(int32_t at, bool first, double v) const {
+        double* p = loc(at);   // off-diagonals always lie in the staged rows
+        *p = first ? 0.0 + v : *p + v;
+    }
+};
+
+// Write the four off-diagonal Jacobian values of one incidence.
+template <class JW>
+__device__ __forceinline__ void inc_offdiag(const IncVals& v, const int4 m, const JW& jw,
+                                            const int32_t rp, const int32_t rq, const int32_t nb) {
+    const bool first = (m.z & FIRST) != 0;
+    const int32_t pos = m.z & POS_MASK;
+    jw.add(rp + pos, first, v.opt);
+    jw.add(rp + nb + pos, first, v.opv);
+    jw.add(rq + pos, first, v.oqt);
+    jw.add(rq + nb + pos, first, v.oqv);
+}
+
+// Sources whose incidence values were computed beforehand (the single-grid
+// incidence phase) set kSplit; the others compute them in place.
 template <class Src, class = void>
-struct PrecomputedIncidences {
+struct SplitIncidences {
     static constexpr bool value = false;
 };
 template <class Src>
-struct PrecomputedIncidences<Src, decltype(void(Src::kPre))> {
-    static constexpr bool value = Src::kPre;
+struct SplitIncidences<Src, decltype(void(Src::kSplit))> {
+    static constexpr bool value = Src::kSplit;
 };
 
 // Operand source of the global-memory path: every read goes to HBM/L2/L1.
@@ -264,13 +308,12 @@ struct GlobalSrc {
 
 // One bus for one scenario (S = PF_LANES: batched lane; S = 1: single grid),
 // operands from `src` (global memory or a shared-memory staging slot).
-template <int MODE, int S, class Src>
+template <int MODE, int S, class Src, class JW>
 __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, const double* tab,
                                                            const int32_t i, const Src& src,
                                                            const Scen<S>& A, const int32_t ln,
-                                                           const int32_t out_l) {
+                                                           const int32_t out_l, const JW& jw) {
     const int32_t N = d.N;
-    double* __restrict__ jv = A.j ? A.j + ln : nullptr;
     const int4 br = src.hdr0();
     const int4 rng = src.hdr1();
     const int32_t rp = br.x, rq = br.y, nb = br.z;
@@ -283,17 +326,26 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
     double d_pt = 0.0, d_pv = 0.0, d_qt = 0.0, d_qv = 0.0;
     unsigned long long nrm = 0;
 
-    for (int32_t e = rng.x; e < rng.y; ++e) {
-        const int32_t t = e - rng.x;
-        const int4 m = src.meta(e, t);
-        if constexpr (PrecomputedIncidences<Src>::value) {
-            inc_apply<MODE, S>(src.vals(e), m, jv, rp, rq, nb, acc_p, acc_q, d_pt, d_pv, d_qt,
-                               d_qv);
-        } else {
+    if constexpr (SplitIncidences<Src>::value) {
+        // values from the incidence phase; it already wrote the off-diagonals
+        // of every SOLO incidence, parallel branches are summed here in order
+        const bool dups = (MODE & JAC) && (br.w & DUPS);
+        for (int32_t e = rng.x; e < rng.y; ++e) {
+            inc_fold<MODE>(src.vals(e), acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
+            if (dups) {
+                const int4 m = src.meta(e, e - rng.x);
+                if (!(m.z & SOLO)) inc_offdiag(src.dup(e), m, jw, rp, rq, nb);
+            }
+        }
+    } else {
+        for (int32_t e = rng.x; e < rng.y; ++e) {
+            const int32_t t = e - rng.x;
+            const int4 m = src.meta(e, t);
             const double tj = src.th_j(m.x, t);
             const double wj = src.v_j(m.x, t);
             const IncVals v = inc_vals<S>(tab, m, src.coef(e, t), th_i, v_i, tj, wj, out_l);
-            inc_apply<MODE, S>(v, m, jv, rp, rq, nb, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
+            inc_fold<MODE>(v, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
+            if (MODE & JAC) inc_offdiag(v, m, jw, rp, rq, nb);
         }
     }
 
@@ -314,8 +366,8 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 nrm = max(nrm, abs_bits(gv));
             }
             if (MODE & JAC) {
-                st_out(jv + dv.z * S, 1.0);   // (g_q[i], Q_g)   kernels.py:244-247
-                st_out(jv + dv.w * S, 1.0);   // (g_V, V_i)
+                jw.put(dv.z, 1.0);   // (g_q[i], Q_g)   kernels.py:244-247
+                jw.put(dv.w, 1.0);   // (g_V, V_i)
             }
         } else if (dv.x == DEV_SLACK) {
             const int32_t q = d.G + k;    // sl_qg, sl_ps are aranges (plan-checked)
@@ -334,10 +386,10 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 nrm = max(nrm, max(abs_bits(gv), abs_bits(gt)));
             }
             if (MODE & JAC) {
-                st_out(jv + dv.z * S, 1.0);                                   // (g_p, P_s)
-                st_out(jv + dv.w * S, 1.0);                                   // (g_q, Q_g)
-                st_out(jv + __ldg(d.gen_row_pos + q) * S, 1.0);               // (g_V, V)
-                st_out(jv + __ldg(d.gen_row_pos + d.n_gen + ps) * S, 1.0);    // (g_theta, theta)
+                jw.put(dv.z, 1.0);                                   // (g_p, P_s)
+                jw.put(dv.w, 1.0);                                   // (g_q, Q_g)
+                jw.put(__ldg(d.gen_row_pos + q), 1.0);               // (g_V, V)
+                jw.put(__ldg(d.gen_row_pos + d.n_gen + ps), 1.0);    // (g_theta, theta)
             }
         } else {  // DEV_SHUNT (kernels.py:236-241, 258-262)
             const double gsh = src.dev_c(dv, t - rng.z), bsh = src.dev_d(dv, t - rng.z);
@@ -358,12 +410,12 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
     nrm = max(nrm, max(abs_bits(acc_p), abs_bits(acc_q)));
     if (MODE & JAC) {
         if (nb > 0) {
-            st_out(jv + (rp + pos_i) * S, d_pt);
-            st_out(jv + (rq + pos_i) * S, d_qt);
+            jw.put(rp + pos_i, d_pt);
+            jw.put(rq + pos_i, d_qt);
         }
         if (vdiag) {
-            st_out(jv + (rp + nb + pos_i) * S, d_pv);
-            st_out(jv + (rq + nb + pos_i) * S, d_qv);
+            jw.put(rp + nb + pos_i, d_pv);
+            jw.put(rq + nb + pos_i, d_qv);
         }
     }
     return nrm;
@@ -374,7 +426,8 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
                                                        const int32_t i, const Scen<S>& A,
                                                        const int32_t ln, const int32_t out_l) {
     GlobalSrc<S> src{d, A, A.y + ln, i, ln};
-    return eval_bus_src<MODE, S>(d, tab, i, src, A, ln, out_l);
+    return eval_bus_src<MODE, S>(d, tab, i, src, A, ln, out_l,
+                                 GlobalJ<S>{A.j ? A.j + ln : nullptr});
 }
 
 // Batched, persistent: gridDim.x CTAs (a few per SM) stride over work items
@@ -466,20 +519,25 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
     if (cur >= 0) flush(cur);
 }
 
-// Single grid, one CTA per grid_buses consecutive buses (their incidences
-// are contiguous), in two phases:
-//   A: threads [B, blockDim) take one incidence each and compute its ten
-//      values into shared memory (all neighbour gathers and trig in
-//      parallel); meanwhile threads [0, B) - one per bus - load the bus
-//      header, own state and first two devices' operands;
-//   B: each bus thread folds its incidences from shared memory in list order
-//      (the reference's association), adds its devices and writes g, the
-//      Jacobian row values and the norm, with no global loads left.
-// The latency chain is ~3 dependent memory round trips per launch instead of
-// one per incidence.
-struct GridSrc : GlobalSrc<1> {
-    static constexpr bool kPre = true;
-    const IncVals* sv;
+// Single grid: one CTA per chunk of consecutive buses (plan-built so that
+// its incidences, Jacobian rows and parallel-branch slots fit the shared-memory
+// caps), in three phases:
+//   0: one thread per bus loads its header, state and first two devices
+//      (registers) and publishes theta, V and the theta-block width;
+//   A: one thread per incidence computes the ten values of its terminal
+//      (pflow kernels.py:79-163) into shared memory and writes its four
+//      off-diagonal Jacobian values into the CTA's staged rows (0.0 + v,
+//      the reference's assembly) unless a parallel branch shares them;
+//   B: each bus thread folds its incidences in list order (the reference's
+//      join and assembly association), adds the parallel-branch values in
+//      order and its devices, and writes g and its diagonal / device values;
+// then the CTA copies its staged rows g_p[b0..b1), g_q[b0..b1) out as two
+// contiguous, coalesced ranges.  A chunk whose single bus exceeds the caps
+// (a hub) is evaluated serially by one thread from global memory.
+struct SingleSrc : GlobalSrc<1> {
+    static constexpr bool kSplit = true;
+    const double* fold;                // [n_inc of chunk][6] {fp, fq, pt, pv, qt, qv}
+    const double* dupv;                // [dup slots][4] {opt, opv, oqt, oqv}
     int32_t E0;
     int4 h0, h1;
     double thi, vi;
@@ -489,7 +547,24 @@ struct GridSrc : GlobalSrc<1> {
     __device__ __forceinline__ int4 hdr1() const { return h1; }
     __device__ __forceinline__ double th_i() const { return thi; }
     __device__ __forceinline__ double v_i() const { return vi; }
-    __device__ __forceinline__ IncVals vals(int32_t e) const { return sv[e - E0]; }
+    __device__ __forceinline__ IncVals vals(int32_t e) const {
+        const double2* p = reinterpret_cast<const double2*>(fold + 6 * (e - E0));
+        const double2 a = p[0], b = p[1], c = p[2];
+        IncVals v;
+        v.fp = a.x; v.fq = a.y;
+        v.pt = b.x; v.pv = b.y;
+        v.qt = c.x; v.qv = c.y;
+        return v;
+    }
+    __device__ __forceinline__ IncVals dup(int32_t e) const {
+        const int32_t slot = (__ldg(&d.sg_inc[e].y) >> SG_DUP_SHIFT) & SG_FIELD_MASK;
+        const double2* p = reinterpret_cast<const double2*>(dupv + 4 * slot);
+        const double2 a = p[0], b = p[1];
+        IncVals v;
+        v.opt = a.x; v.opv = a.y;
+        v.oqt = b.x; v.oqv = b.y;
+        return v;
+    }
     __device__ __forceinline__ int4 dev(int32_t t, int32_t u) const {
         return u == 0 ? dv0 : u == 1 ? dv1 : GlobalSrc<1>::dev(t, u);
     }
@@ -509,9 +584,9 @@ struct GridSrc : GlobalSrc<1> {
 
 // load device u's record and operands into registers (types it does not use
 // are left untouched: no out-of-range reads)
-__device__ __forceinline__ void grid_dev(const GlobalSrc<1>& gs, const DevicePlan& d, int32_t t,
-                                         bool have, int4& dv, double& a, double& b, double& c,
-                                         double& dd) {
+__device__ __forceinline__ void single_dev(const GlobalSrc<1>& gs, const DevicePlan& d, int32_t t,
+                                           bool have, int4& dv, double& a, double& b, double& c,
+                                           double& dd) {
     dv = have ? __ldg(d.dev_list + t) : make_int4(-1, 0, 0, 0);
     a = b = c = dd = 0.0;
     if (dv.x == DEV_PQ || dv.x == DEV_PV || dv.x == DEV_SLACK) {
@@ -522,70 +597,143 @@ __device__ __forceinline__ void grid_dev(const GlobalSrc<1>& gs, const DevicePla
     if (dv.x == DEV_SLACK || dv.x == DEV_SHUNT) dd = gs.dev_d(dv, 0);
 }
 
+// shared-memory layout of k_eval_single (doubles, then ints)
+constexpr int SG_SMEM_FOLD = 0;
+constexpr int SG_SMEM_DUP = SG_SMEM_FOLD + 6 * SG_CAP_INC;
+constexpr int SG_SMEM_J = SG_SMEM_DUP + 4 * SG_CAP_DUP;
+constexpr int SG_SMEM_TH = SG_SMEM_J + SG_CAP_J;
+constexpr int SG_SMEM_V = SG_SMEM_TH + SG_CAP_BUS;
+constexpr int SG_SMEM_DOUBLES = SG_SMEM_V + SG_CAP_BUS;
+constexpr size_t SG_SMEM_BYTES = 8 * (size_t)SG_SMEM_DOUBLES + 4 * (size_t)SG_CAP_BUS;
+
+// CTA max -> one integer atomicMax of the |g| bit pattern into the plan's
+// accumulator (exact, order-independent); the last CTA moves it to *norm and
+// re-arms accumulator and counter for the next launch.  Thread 0 only, after
+// a barrier; release / acquire atomics order the max before the count.
+__device__ __forceinline__ unsigned long long single_norm(const DevicePlan& d,
+                                                          unsigned long long nrm,
+                                                          unsigned long long* red,
+                                                          unsigned long long* norm) {
+    for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long mx = red[0];
+        for (int w = 1; w < SG_THREADS / 32; ++w) mx = max(mx, red[w]);
+        atomicMax(d.sg_acc, mx);
+        unsigned int done;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(done) : "l"(d.sg_count) : "memory");
+        if (done == gridDim.x - 1) {
+            unsigned long long v;
+            asm volatile("atom.acquire.gpu.global.exch.b64 %0, [%1], 0;"
+                         : "=l"(v) : "l"(d.sg_acc) : "memory");
+            *norm = v;
+            *d.sg_count = 0;
+        }
+    }
+    return nrm;
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(128) k_eval_single(const DevicePlan d,
-                                                     const double* __restrict__ y,
-                                                     double* __restrict__ g,
-                                                     double* __restrict__ jv,
-                                                     unsigned long long* __restrict__ norm) {
-    extern __shared__ __align__(16) unsigned char grid_smem[];
-    IncVals* sv = reinterpret_cast<IncVals*>(grid_smem);
-    __shared__ unsigned long long red[4];
+__global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const DevicePlan d,
+                                                            const double* __restrict__ y,
+                                                            double* __restrict__ g,
+                                                            double* __restrict__ jv,
+                                                            unsigned long long* __restrict__ norm) {
+    extern __shared__ __align__(16) double sg[];
+    __shared__ unsigned long long red[SG_THREADS / 32];
     __shared__ double s_tab[PF_TRIG_N * 4];
     const double* tab = stage_trig_table(s_tab);
-    const int32_t N = d.N, B = d.grid_buses;
-    const int32_t b0 = blockIdx.x * B, b1 = min(N, b0 + B);
-    const int32_t E0 = __ldg(d.inc_ptr + b0), E1 = __ldg(d.inc_ptr + b1);
-    const int32_t i = b0 + threadIdx.x;
-    const bool own = threadIdx.x < B && i < b1;
-    Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
-    GridSrc src{{d, A, y, i, 0}, sv, E0, make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0), 0.0, 0.0};
-    if (own) {
-        src.h0 = __ldg(d.bus_row + 2 * i);
-        src.h1 = __ldg(d.bus_row + 2 * i + 1);
-        src.thi = __ldg(y + i);
-        src.vi = __ldg(y + N + i);
-        const int32_t t0 = src.h1.z, nd = src.h1.w - src.h1.z;
-        grid_dev(src, d, t0, nd > 0, src.dv0, src.a0, src.b0, src.c0, src.d0);
-        grid_dev(src, d, t0 + 1, nd > 1, src.dv1, src.a1, src.b1, src.c1, src.d1);
-    }
-    const int32_t nA = blockDim.x - B;
-    for (int32_t e = E0 + (int32_t)threadIdx.x - B; threadIdx.x >= B && e < E1; e += nA) {
-        const int4 m = __ldg(d.inc_meta + e);
-        const double4 c = ldg4(d.inc_coef + e);
-        const int32_t o = m.w;
-        sv[e - E0] = inc_vals<1>(tab, m, c, __ldg(y + o), __ldg(y + N + o), __ldg(y + m.x),
-                                 __ldg(y + N + m.x), -1);
-    }
-    __syncthreads();
+    const int32_t N = d.N;
+    const int t = threadIdx.x;
+    const int4 c0 = __ldg(d.sg_chunk + 2 * blockIdx.x);
+    const int32_t b0 = c0.x, b1 = c0.y & ~SG_BIG, E0 = c0.z, E1 = c0.w;
+    const Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
     unsigned long long nrm = 0;
-    if (own) nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1);
-    if (MODE & NORM) {
-        // per-CTA max into the plan's scratch; the last CTA to finish reduces
-        // them and re-arms the counter, so no separate zeroing launch is needed
-        for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
-        __syncthreads();
-        __shared__ bool last;
-        if (threadIdx.x == 0) {
-            d.norm_part[blockIdx.x] = max(max(red[0], red[1]), max(red[2], red[3]));
-            __threadfence();
-            last = atomicAdd(d.norm_count, 1u) == gridDim.x - 1;
+    if (c0.y & SG_BIG) {
+        if (t == 0) nrm = eval_bus<MODE, 1>(d, tab, b0, A, 0, -1);
+    } else {
+        const int4 c1 = __ldg(d.sg_chunk + 2 * blockIdx.x + 1);
+        double* fold = sg + SG_SMEM_FOLD;
+        double* dupv = sg + SG_SMEM_DUP;
+        double* jst = sg + SG_SMEM_J;
+        double* bth = sg + SG_SMEM_TH;
+        double* bv = sg + SG_SMEM_V;
+        int32_t* bnb = reinterpret_cast<int32_t*>(sg + SG_SMEM_DOUBLES);
+        const int32_t i = b0 + t;
+        const bool own = i < b1;
+        // the first incidence's operands do not depend on phase 0: issue
+        // their loads before it so the two latency chains overlap
+        const int32_t ea = E0 + t;
+        int4 ra = make_int4(0, 0, 0, 0);
+        double4 ca = make_double4(0.0, 0.0, 0.0, 0.0);
+        double tja = 0.0, wja = 0.0;
+        if (ea < E1) {
+            ra = __ldg(d.sg_inc + ea);
+            ca = ldg4(d.inc_coef + ea);
+            tja = __ldg(y + ra.x);
+            wja = __ldg(y + N + ra.x);
+        }
+        SingleSrc src{{d, A, y, i, 0}, fold, dupv, E0, make_int4(0, 0, 0, 0),
+                      make_int4(0, 0, 0, 0), 0.0, 0.0};
+        if (own) {   // phase 0
+            src.h0 = __ldg(d.bus_row + 2 * i);
+            src.h1 = __ldg(d.bus_row + 2 * i + 1);
+            src.thi = __ldg(y + i);
+            src.vi = __ldg(y + N + i);
+            bth[t] = src.thi;
+            bv[t] = src.vi;
+            bnb[t] = src.h0.z;
+            const int32_t t0 = src.h1.z, nd = src.h1.w - src.h1.z;
+            single_dev(src, d, t0, nd > 0, src.dv0, src.a0, src.b0, src.c0, src.d0);
+            single_dev(src, d, t0 + 1, nd > 1, src.dv1, src.a1, src.b1, src.c1, src.d1);
         }
         __syncthreads();
-        if (last) {
-            __threadfence();
-            unsigned long long mx = 0;
-            for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x)
-                mx = max(mx, __ldcg(d.norm_part + b));
-            for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                *norm = max(max(red[0], red[1]), max(red[2], red[3]));
-                *d.norm_count = 0;
+        auto incidence = [&](int32_t e, int4 r, double4 c, double tj, double wj) {   // phase A
+            const int32_t o = r.y & SG_FIELD_MASK;
+            const int4 m = make_int4(r.x, -1, r.y & KSIDE, 0);
+            const IncVals v = inc_vals<1>(tab, m, c, bth[o], bv[o], tj, wj, -1);
+            double2* f = reinterpret_cast<double2*>(fold + 6 * (e - E0));
+            if (MODE & (RES | NORM)) f[0] = make_double2(v.fp, v.fq);
+            if (MODE & JAC) {
+                f[1] = make_double2(v.pt, v.pv);
+                f[2] = make_double2(v.qt, v.qv);
+                if (r.y & SOLO) {
+                    const int32_t w = bnb[o];
+                    jst[r.z] = 0.0 + v.opt;
+                    jst[r.z + w] = 0.0 + v.opv;
+                    jst[r.w] = 0.0 + v.oqt;
+                    jst[r.w + w] = 0.0 + v.oqv;
+                } else {
+                    double2* u = reinterpret_cast<double2*>(
+                        dupv + 4 * ((r.y >> SG_DUP_SHIFT) & SG_FIELD_MASK));
+                    u[0] = make_double2(v.opt, v.opv);
+                    u[1] = make_double2(v.oqt, v.oqv);
+                }
             }
+        };
+        if (ea < E1) incidence(ea, ra, ca, tja, wja);
+        for (int32_t e = ea + SG_THREADS; e < E1; e += SG_THREADS) {
+            const int4 r = __ldg(d.sg_inc + e);
+            incidence(e, r, ldg4(d.inc_coef + e), __ldg(y + r.x), __ldg(y + N + r.x));
         }
+        __syncthreads();
+        if (own)   // phase B
+            nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1,
+                                        StagedJ{jst, jv, c1.x, c1.y, c1.z, c1.w});
+        if (MODE & (JAC | NORM)) __syncthreads();
+        if (MODE & NORM) nrm = single_norm(d, nrm, red, norm);
+        if (MODE & JAC) {   // staged rows out as two contiguous ranges
+            const int32_t lp = c1.y - c1.x, lq = c1.w - c1.z;
+            for (int32_t k = t; k < lp; k += SG_THREADS) jv[c1.x + k] = jst[k];
+            for (int32_t k = t; k < lq; k += SG_THREADS) jv[c1.z + k] = jst[lp + k];
+        }
+        return;
+    }
+    if (MODE & NORM) {
+        __syncthreads();
+        single_norm(d, nrm, red, norm);
     }
 }
 
@@ -780,14 +928,13 @@ inline unsigned grid_for(int64_t n, int threads) {
 template <int MODE>
 static void launch_single_mode(const DevicePlan& d, const double* y, double* g, double* j,
                                double* norm, cudaStream_t st) {
-    const size_t smem = sizeof(IncVals) * (size_t)std::max(d.grid_max_inc, 1);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    static bool configured = false;
+    if (!configured) {
         cudaFuncSetAttribute(k_eval_single<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        configured = smem;
+                             (int)SG_SMEM_BYTES);
+        configured = true;
     }
-    k_eval_single<MODE><<<grid_for(d.N, d.grid_buses), 128, smem, st>>>(
+    k_eval_single<MODE><<<d.sg_chunks, SG_THREADS, SG_SMEM_BYTES, st>>>(
         d, y, g, j, reinterpret_cast<unsigned long long*>(norm));
 }
 

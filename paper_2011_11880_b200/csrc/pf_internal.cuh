@@ -13,17 +13,33 @@ namespace pf {
 // Per-incidence metadata flag bits (inc_meta.z).
 constexpr int32_t KSIDE = 1 << 30;   // this bus is the branch's k (to) terminal
 constexpr int32_t FIRST = 1 << 29;   // first incidence of this neighbour in the bus's list
-constexpr int32_t POS_MASK = (1 << 29) - 1;
+constexpr int32_t SOLO = 1 << 28;    // the only incidence of this neighbour (no parallel branch)
+constexpr int32_t POS_MASK = (1 << 28) - 1;
 
-// Per-bus row descriptor (bus_row.w flag bit).
+// Per-bus row descriptor (bus_row.w flag bits).
 constexpr int32_t VDIAG = 1 << 30;   // row holds a (g, V_i) diagonal entry
+constexpr int32_t DUPS = 1 << 29;    // some neighbour is reached by parallel branches
 
 // buses with at least this many incidences are scheduled first (batched)
 constexpr int HUB_DEG = 16;
 
-// shared-memory bytes per incidence in the single-grid two-phase kernel
-constexpr int GRID_INC_VALS = 10;
-constexpr int GRID_INC_BYTES = 8 * GRID_INC_VALS;
+// Single grid (k_eval_single): one CTA of SG_THREADS per chunk of at most
+// SG_THREADS consecutive buses whose incidences, Jacobian rows g_p / g_q and
+// parallel-branch slots fit the shared-memory caps below (plan-built).
+constexpr int SG_THREADS = 128;
+// 5 CTAs per SM (<= 102 registers): config 2's ~700 chunks run in one wave.
+// Measured on B200 (config 2, f+J+norm): 4 CTAs 15.0 us, 5 CTAs 10.2 us,
+// 6 CTAs (80 registers, spills) 13.2 us; 256-thread CTAs 14.2-15.2 us.
+constexpr int SG_MINB = 5;
+constexpr int SG_CAP_BUS = SG_THREADS;
+constexpr int SG_CAP_INC = 2 * SG_THREADS;   // incidences per chunk (two per thread)
+constexpr int SG_CAP_J = 16 * SG_THREADS;    // Jacobian values in the chunk's rows g_p, g_q
+constexpr int SG_CAP_DUP = SG_THREADS / 4;   // incidences sharing a neighbour with a parallel branch
+constexpr int32_t SG_BIG = 1 << 30;  // chunk flag: one bus over the caps, evaluated serially
+// sg_inc.y: owner bus (chunk-local, bits 0-9) | dup slot << SG_DUP_SHIFT | SOLO | KSIDE
+constexpr int32_t SG_FIELD_MASK = 0x3ff;
+constexpr int SG_DUP_SHIFT = 10;
+static_assert(SG_CAP_BUS <= SG_FIELD_MASK + 1 && SG_CAP_DUP <= SG_FIELD_MASK + 1, "sg_inc");
 
 // Device-list entry types, in the reference's pool-segment order (residual.py:57).
 enum DevType : int32_t { DEV_PQ = 0, DEV_PV = 1, DEV_SLACK = 2, DEV_SHUNT = 3 };
@@ -31,10 +47,15 @@ enum DevType : int32_t { DEV_PQ = 0, DEV_PV = 1, DEV_SLACK = 2, DEV_SHUNT = 3 };
 // Everything the evaluation kernels read.  All pointers are device memory.
 struct DevicePlan {
     int32_t N, L, P, G, S, H, n_gen, n_var, nnz, n_inc;
-    int32_t grid_buses, grid_max_inc;   // single-grid two-phase kernel partition
-    // single-grid norm: per-CTA maxima and a completion counter (last CTA reduces)
-    unsigned long long* norm_part;      // [grid_for(N, grid_buses)]
-    unsigned int* norm_count;           // 0 between launches
+    // single grid: chunk records [2 sg_chunks]: {b0, b1 | SG_BIG, e0, e1},
+    // {p0, p1, q0, q1} (CSR ranges of rows g_p[b0..b1), g_q[b0..b1)), and per
+    // incidence {neighbour, sg_inc.y fields, staged position of the
+    // (g_p[i], theta_j) entry, staged position of the (g_q[i], theta_j) entry}
+    int32_t sg_chunks;
+    const int4* sg_chunk;
+    const int4* sg_inc;
+    unsigned long long* sg_acc;   // norm accumulator, 0 between launches
+    unsigned int* sg_count;       // CTAs done, 0 between launches
     // incidence lists: bus i owns [inc_ptr[i], inc_ptr[i+1]) in the order
     // (branches with h=i ascending) ++ (branches with k=i ascending)
     const int32_t* inc_ptr;   // [N+1]

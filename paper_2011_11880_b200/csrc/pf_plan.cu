@@ -146,7 +146,9 @@ __global__ void k_nbr_ranks(int64_t m, int32_t n_inc, const unsigned long long* 
     if (head[u]) ucol[uq] = col;
     int32_t pos = uq - ubase[bus];
     int32_t v = vals[u];
-    if (v < n_inc) meta[v].z |= pos | (head[u] ? FIRST : 0);
+    // SOLO: the only incidence of this (bus, neighbour) pair
+    const bool solo = head[u] && (u + 1 == m || keys[u + 1] != keys[u]);
+    if (v < n_inc) meta[v].z |= pos | (head[u] ? FIRST : 0) | (solo ? SOLO : 0);
     else pos_i[bus] = pos;
 }
 
@@ -249,7 +251,11 @@ __global__ void k_fill(int32_t N, int32_t n_gen, const int32_t* ubase, const int
         }
         dev_list[u] = ent;
     }
-    bus_row[2 * i] = make_int4((int32_t)rp, (int32_t)rq, nb, pos_i[i] | (nv > 0 ? VDIAG : 0));
+    // parallel branches: more incidences than distinct neighbours (the theta
+    // block also holds the bus itself)
+    const bool dups = nb > 0 && inc_ptr[i + 1] - inc_ptr[i] > nb - 1;
+    bus_row[2 * i] = make_int4((int32_t)rp, (int32_t)rq, nb,
+                               pos_i[i] | (nv > 0 ? VDIAG : 0) | (dups ? DUPS : 0));
     bus_row[2 * i + 1] = make_int4(inc_ptr[i], inc_ptr[i + 1], dev_ptr[i], dev_ptr[i + 1]);
 }
 
@@ -611,25 +617,75 @@ int build(const pf_topology* t, pf_plan** out) {
                           cudaMemcpyHostToDevice));
         d.bus_order = bus_order;
     }
-    // single-grid two-phase kernel: buses per CTA and the largest incidence
-    // count of any CTA (sizes its shared-memory staging)
-    d.grid_buses = 32;
-    for (int B : {32, 16, 8}) {
-        int32_t mx = 0;
-        for (int32_t b0 = 0; b0 < N; b0 += B) mx = std::max(mx, hptr[std::min(N, b0 + B)] - hptr[b0]);
-        d.grid_buses = B;
-        d.grid_max_inc = mx;
-        if ((int64_t)mx * GRID_INC_BYTES <= 96 * 1024) break;
-    }
-    // single-grid norm scratch (the counter must start at zero)
+    // single-grid chunks (k_eval_single): consecutive buses while the
+    // incidences, the Jacobian values of rows g_p / g_q and the parallel-branch
+    // slots fit the shared-memory caps; a lone bus over a cap is flagged SG_BIG
     {
-        unsigned long long* part;
+        std::vector<int4> hmeta(n_inc), hrow(2 * (size_t)N);
+        std::vector<int64_t> hip(n_var + 1);
+        PF_TRY(cudaMemcpy(hmeta.data(), meta, sizeof(int4) * (size_t)n_inc, cudaMemcpyDeviceToHost));
+        PF_TRY(cudaMemcpy(hrow.data(), bus_row, sizeof(int4) * 2 * (size_t)N,
+                          cudaMemcpyDeviceToHost));
+        PF_TRY(cudaMemcpy(hip.data(), indptr64, sizeof(int64_t) * (size_t)(n_var + 1),
+                          cudaMemcpyDeviceToHost));
+        std::vector<int4> chunks, sginc(n_inc, make_int4(0, 0, 0, 0));
+        auto jrows = [&](int32_t i) {
+            return (hip[i + 1] - hip[i]) + (hip[N + i + 1] - hip[N + i]);
+        };
+        auto ndups = [&](int32_t i) {
+            int32_t c = 0;
+            for (int32_t e = hptr[i]; e < hptr[i + 1]; ++e) c += !(hmeta[e].z & SOLO);
+            return c;
+        };
+        for (int32_t b0 = 0; b0 < N;) {
+            int32_t b1 = b0;
+            int64_t ninc = 0, nj = 0, ndup = 0;
+            while (b1 < N && b1 - b0 < SG_CAP_BUS) {
+                const int64_t di = hptr[b1 + 1] - hptr[b1], ji = jrows(b1), ui = ndups(b1);
+                if (b1 > b0 && (ninc + di > SG_CAP_INC || nj + ji > SG_CAP_J ||
+                                ndup + ui > SG_CAP_DUP))
+                    break;
+                ninc += di;
+                nj += ji;
+                ndup += ui;
+                ++b1;
+            }
+            const bool big = ninc > SG_CAP_INC || nj > SG_CAP_J || ndup > SG_CAP_DUP;
+            const int32_t p0 = (int32_t)hip[b0], p1 = (int32_t)hip[b1];
+            const int32_t q0 = (int32_t)hip[N + b0], q1 = (int32_t)hip[N + b1];
+            chunks.push_back(make_int4(b0, b1 | (big ? SG_BIG : 0), hptr[b0], hptr[b1]));
+            chunks.push_back(make_int4(p0, p1, q0, q1));
+            int32_t slot = 0;
+            for (int32_t e = hptr[b0]; !big && e < hptr[b1]; ++e) {
+                const int4 m = hmeta[e];
+                const int32_t own = m.w, pos = m.z & POS_MASK;
+                const int4 r = hrow[2 * (size_t)own];
+                int32_t f = (own - b0) | (m.z & (SOLO | KSIDE));
+                if (!(m.z & SOLO)) f |= slot++ << SG_DUP_SHIFT;
+                sginc[e] = make_int4(m.x, f, r.x + pos - p0, r.y + pos - q0 + (p1 - p0));
+            }
+            b0 = b1;
+        }
+        int4 *dchunk, *dinc;
+        unsigned long long* acc;
         unsigned int* cnt;
-        PF_TRY(owned_alloc(P, &part, (N + d.grid_buses - 1) / d.grid_buses + 1));
+        PF_TRY(owned_alloc(P, &dchunk, (int64_t)chunks.size()));
+        PF_TRY(owned_alloc(P, &dinc, n_inc));
+        PF_TRY(owned_alloc(P, &acc, 1));
         PF_TRY(owned_alloc(P, &cnt, 1));
+        if (!chunks.empty())
+            PF_TRY(cudaMemcpy(dchunk, chunks.data(), sizeof(int4) * chunks.size(),
+                              cudaMemcpyHostToDevice));
+        if (n_inc)
+            PF_TRY(cudaMemcpy(dinc, sginc.data(), sizeof(int4) * (size_t)n_inc,
+                              cudaMemcpyHostToDevice));
+        PF_TRY(cudaMemset(acc, 0, sizeof(unsigned long long)));
         PF_TRY(cudaMemset(cnt, 0, sizeof(unsigned int)));
-        d.norm_part = part;
-        d.norm_count = cnt;
+        d.sg_chunks = (int32_t)(chunks.size() / 2);
+        d.sg_chunk = dchunk;
+        d.sg_inc = dinc;
+        d.sg_acc = acc;
+        d.sg_count = cnt;
     }
     count_launch(12);
     *out = P;
