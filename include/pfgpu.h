@@ -109,9 +109,9 @@ PF_API int pf_plan_pattern_csc(const pf_plan* plan, int32_t* csc_indptr, int32_t
  * y[n_var] -> g[n_eq] (pflow evaluate_residual, residual.py:262-274),
  * jval[nnz] CSR-ordered values (pflow evaluate_jacobian, jacobian.py:216-221),
  * norm[1] = max|g| (pflow/newton.py:84-85).  Any output may be NULL to skip it.
- * Two launches (branch pass, bus pass) that hand off through plan-owned
- * buffers: single-grid evaluations of one plan must not run concurrently
- * (different plans may; batched evaluations are unaffected). */
+ * One launch.  The norm reduction uses a plan-owned accumulator: evaluations
+ * of one plan that request `norm` must not run concurrently (different plans
+ * may; batched evaluations are unaffected). */
 PF_API int pf_eval(const pf_plan* plan, const double* y, double* g, double* jval, double* norm,
             void* stream);
 
