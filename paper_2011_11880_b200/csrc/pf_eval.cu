@@ -610,6 +610,8 @@ constexpr size_t SG_SMEM_BYTES = 8 * (size_t)SG_SMEM_DOUBLES + 4 * (size_t)SG_CA
 // accumulator (exact, order-independent); the last CTA moves it to *norm and
 // re-arms accumulator and counter for the next launch.  Thread 0 only, after
 // a barrier; release / acquire atomics order the max before the count.
+// (A memset of *norm before the launch plus a plain atomicMax measured
+// 2.5 us slower per evaluation inside a CUDA graph.)
 __device__ __forceinline__ unsigned long long single_norm(const DevicePlan& d,
                                                           unsigned long long nrm,
                                                           unsigned long long* red,
@@ -644,17 +646,29 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
     extern __shared__ __align__(16) double sg[];
     __shared__ unsigned long long red[SG_THREADS / 32];
     __shared__ double s_tab[PF_TRIG_N * 4];
-    const double* tab = stage_trig_table(s_tab);
     const int32_t N = d.N;
     const int t = threadIdx.x;
+    // Every global access is a ~0.5 us round trip here (one wave, one
+    // dependent chain per CTA), so loads are issued level by level: chunk
+    // record and trig table first, then everything that depends only on
+    // the chunk record, and the table reaches shared memory at the first
+    // barrier (it is not read before).
     const int4 c0 = __ldg(d.sg_chunk + 2 * blockIdx.x);
+    const int4 c1 = __ldg(d.sg_chunk + 2 * blockIdx.x + 1);
+    constexpr int TAB = PF_TRIG_N * 4;
+    static_assert(TAB <= 2 * SG_THREADS, "trig table staging");
+    const double tv0 = __ldg(pf_trig_tab + t);
+    const double tv1 = t + SG_THREADS < TAB ? __ldg(pf_trig_tab + t + SG_THREADS) : 0.0;
+    const double* tab = s_tab;
     const int32_t b0 = c0.x, b1 = c0.y & ~SG_BIG, E0 = c0.z, E1 = c0.w;
     const Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
     unsigned long long nrm = 0;
     if (c0.y & SG_BIG) {
+        s_tab[t] = tv0;
+        if (t + SG_THREADS < TAB) s_tab[t + SG_THREADS] = tv1;
+        __syncthreads();
         if (t == 0) nrm = eval_bus<MODE, 1>(d, tab, b0, A, 0, -1);
     } else {
-        const int4 c1 = __ldg(d.sg_chunk + 2 * blockIdx.x + 1);
         double* fold = sg + SG_SMEM_FOLD;
         double* dupv = sg + SG_SMEM_DUP;
         double* jst = sg + SG_SMEM_J;
@@ -663,25 +677,31 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         int32_t* bnb = reinterpret_cast<int32_t*>(sg + SG_SMEM_DOUBLES);
         const int32_t i = b0 + t;
         const bool own = i < b1;
-        // the first incidence's operands do not depend on phase 0: issue
-        // their loads before it so the two latency chains overlap
+        // level 2: the first incidence's record and the bus header / state
         const int32_t ea = E0 + t;
         int4 ra = make_int4(0, 0, 0, 0);
         double4 ca = make_double4(0.0, 0.0, 0.0, 0.0);
-        double tja = 0.0, wja = 0.0;
         if (ea < E1) {
             ra = __ldg(d.sg_inc + ea);
             ca = ldg4(d.inc_coef + ea);
-            tja = __ldg(y + ra.x);
-            wja = __ldg(y + N + ra.x);
         }
         SingleSrc src{{d, A, y, i, 0}, fold, dupv, E0, make_int4(0, 0, 0, 0),
                       make_int4(0, 0, 0, 0), 0.0, 0.0};
-        if (own) {   // phase 0
+        if (own) {
             src.h0 = __ldg(d.bus_row + 2 * i);
             src.h1 = __ldg(d.bus_row + 2 * i + 1);
             src.thi = __ldg(y + i);
             src.vi = __ldg(y + N + i);
+        }
+        s_tab[t] = tv0;
+        if (t + SG_THREADS < TAB) s_tab[t + SG_THREADS] = tv1;
+        // level 3: the neighbour's state; devices (record, then operands)
+        double tja = 0.0, wja = 0.0;
+        if (ea < E1) {
+            tja = __ldg(y + ra.x);
+            wja = __ldg(y + N + ra.x);
+        }
+        if (own) {   // phase 0
             bth[t] = src.thi;
             bv[t] = src.vi;
             bnb[t] = src.h0.z;
