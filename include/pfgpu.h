@@ -83,6 +83,8 @@ typedef struct pf_plan pf_plan;
 enum {
     PF_DIM_NBUS = 0, PF_DIM_NLINE, PF_DIM_NVAR, PF_DIM_NNZ, PF_DIM_NPQ,
     PF_DIM_NPV, PF_DIM_NSLACK, PF_DIM_NSHUNT, PF_DIM_NINC, PF_DIM_MAXDEG,
+    PF_DIM_SG_CHUNKS,   /* single-grid CTAs (bus chunks) */
+    PF_DIM_SG_BIG,      /* of which single over-cap buses evaluated serially */
     PF_DIM_COUNT
 };
 

@@ -18,7 +18,8 @@ LIB_PATH = PKG_DIR / "libpfgpu.so"
 PF_OK, PF_EINVAL, PF_ECUDA, PF_ESHAPE, PF_ENOMEM = 0, 1, 2, 3, 4
 PF_LANES = 32
 (PF_DIM_NBUS, PF_DIM_NLINE, PF_DIM_NVAR, PF_DIM_NNZ, PF_DIM_NPQ, PF_DIM_NPV,
- PF_DIM_NSLACK, PF_DIM_NSHUNT, PF_DIM_NINC, PF_DIM_MAXDEG, PF_DIM_COUNT) = range(11)
+ PF_DIM_NSLACK, PF_DIM_NSHUNT, PF_DIM_NINC, PF_DIM_MAXDEG, PF_DIM_SG_CHUNKS, PF_DIM_SG_BIG,
+ PF_DIM_COUNT) = range(13)
 
 _I32P = C.POINTER(C.c_int32)
 _F64P = C.POINTER(C.c_double)

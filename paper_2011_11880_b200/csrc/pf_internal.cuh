@@ -105,6 +105,7 @@ struct Staging {
 struct pf_plan {
     pf::DevicePlan d;
     int32_t max_deg = 0;
+    int32_t sg_big = 0;     // single-grid chunks evaluated serially (one over-cap bus)
     void* owned[96] = {};   // device allocations to free
     int n_owned = 0;
     // single-grid host drop-in staging

@@ -682,6 +682,8 @@ int build(const pf_topology* t, pf_plan** out) {
         PF_TRY(cudaMemset(acc, 0, sizeof(unsigned long long)));
         PF_TRY(cudaMemset(cnt, 0, sizeof(unsigned int)));
         d.sg_chunks = (int32_t)(chunks.size() / 2);
+        P->sg_big = 0;
+        for (size_t c = 0; c < chunks.size(); c += 2) P->sg_big += (chunks[c].y & SG_BIG) != 0;
         d.sg_chunk = dchunk;
         d.sg_inc = dinc;
         d.sg_acc = acc;
@@ -735,6 +737,8 @@ int pf_plan_dims(const pf_plan* p, int64_t* dims) {
     dims[PF_DIM_NSHUNT] = d.H;
     dims[PF_DIM_NINC] = d.n_inc;
     dims[PF_DIM_MAXDEG] = p->max_deg;
+    dims[PF_DIM_SG_CHUNKS] = d.sg_chunks;
+    dims[PF_DIM_SG_BIG] = p->sg_big;
     return PF_OK;
 }
 

@@ -83,6 +83,8 @@ class Plan:
         self.n_slack = dims[_abi.PF_DIM_NSLACK]
         self.n_shunt = dims[_abi.PF_DIM_NSHUNT]
         self.max_degree = dims[_abi.PF_DIM_MAXDEG]
+        self.single_chunks = dims[_abi.PF_DIM_SG_CHUNKS]      # single-grid CTAs
+        self.single_serial = dims[_abi.PF_DIM_SG_BIG]         # over-cap buses done serially
 
     def close(self) -> None:
         if getattr(self, "_h", None):

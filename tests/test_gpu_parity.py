@@ -432,3 +432,74 @@ def test_random_grids_fuzz(seed):
     assert_parity(G, from_blocked(gr, K, plan.n_var), "batched g")
     assert_parity(J[:, perm], from_blocked(jr, K, plan.nnz), "batched J")
     assert np.array_equal(nr[:K].cpu().numpy(), np.abs(G).max(axis=1))
+
+
+def _chunking_case():
+    """Single-grid chunk edge cases: a hub of degree ~350 (over the incidence
+    cap), a bus pair joined by 40 parallel branches (over the parallel-branch
+    cap), several buses with many generators, and dense neighbourhoods that
+    split chunks on the Jacobian cap."""
+    from paper_2011_11880_b200 import case as C
+
+    rng = np.random.default_rng(77)
+    nb = 600
+    ids = np.arange(1, nb + 1)
+    btype = np.ones(nb, dtype=np.int64)
+    btype[0] = 3
+    btype[20:60] = 2
+    fr, to = [], []
+    for i in range(1, nb):                          # chain keeps it connected
+        fr.append(i), to.append(i + 1)
+    for k in range(100, 450):                        # hub at bus 5
+        fr.append(5), to.append(k)
+    for _ in range(40):                              # 40 parallel branches 10-11
+        fr.append(10), to.append(11)
+    for _ in range(3):                               # reversed parallels 12-13
+        fr.append(13), to.append(12)
+    for _ in range(900):                             # dense block 460..520
+        a, b = rng.choice(np.arange(460, 521), 2, replace=False)
+        fr.append(int(a)), to.append(int(b))
+    L = len(fr)
+    bus = dict(bus_id=ids, bus_type=btype, pd=rng.uniform(0, 50, nb), qd=rng.uniform(0, 20, nb),
+               gs=np.where(rng.uniform(size=nb) < 0.1, 2.0, 0.0),
+               bs=np.where(rng.uniform(size=nb) < 0.1, 5.0, 0.0),
+               vm=np.ones(nb), va=np.zeros(nb), base_kv=np.full(nb, 230.0))
+    gbus = [1] + [int(b) for b in range(21, 61)] + [25] * 6 + [30] * 5
+    ng = len(gbus)
+    gen = dict(gen_bus=gbus, pg=rng.uniform(10, 90, ng), qg=np.zeros(ng), qmax=np.full(ng, 99.0),
+               qmin=np.full(ng, -99.0), vg=rng.uniform(0.98, 1.05, ng), gen_status=np.ones(ng))
+    branch = dict(from_bus=fr, to_bus=to, r=rng.uniform(0.001, 0.05, L),
+                  x=rng.uniform(0.01, 0.3, L), b=rng.uniform(0, 0.1, L),
+                  ratio=np.where(rng.uniform(size=L) < 0.2, rng.uniform(0.95, 1.05, L), 1.0),
+                  angle=np.where(rng.uniform(size=L) < 0.1, rng.uniform(-5, 5, L), 0.0),
+                  br_status=np.ones(L))
+    return C.make_case(100.0, bus, gen, branch, name="chunking")
+
+
+def test_single_grid_chunk_caps_vs_oracle():
+    """Over-cap buses take the serial path (plan.single_serial > 0), caps
+    split the other chunks; values and norm still match the oracle."""
+    s = build_system(_chunking_case())
+    plan = _plan(s)
+    assert plan.max_degree >= 300
+    assert plan.single_serial >= 2          # the hub and the 40-way parallel pair
+    assert plan.single_chunks > plan.single_serial
+    o = oracle.Oracle(s)
+    cptr, cidx = o.pattern_csc()
+    pptr, pidx, perm = plan.pattern_csc()
+    assert np.array_equal(cptr, pptr) and np.array_equal(cidx, pidx)
+    for k in range(3):
+        y = random_state(s, 500 + k)
+        g, j, norm = _eval(plan, y)
+        g_ref = o.residual(y)
+        assert_parity(g, g_ref, "g")
+        assert_parity(j[perm], o.jacobian(y), "J")
+        assert norm == np.abs(g).max()
+        # residual-only and Jacobian-only launches agree with the fused one
+        gg = plan.empty(plan.n_var)
+        plan.eval(_dev(y), g=gg)
+        jj = plan.empty(plan.nnz)
+        plan.eval(_dev(y), jval=jj)
+        torch.cuda.synchronize()
+        assert np.array_equal(gg[: plan.n_var].cpu().numpy(), g)
+        assert np.array_equal(jj[: plan.nnz].cpu().numpy(), j)
