@@ -979,12 +979,12 @@ cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, 
     return cudaGetLastError();
 }
 
-constexpr int BATCH_W = 8;
-
-// 8 warps per CTA, 3 CTAs per SM (80 registers, no spills).  Measured
-// alternatives on B200: 2 CTAs (more registers) and 4 CTAs (64 registers,
-// spills) were both slower.
-constexpr int BATCH_MINB = 3;
+// 12 warps per CTA, 2 CTAs per SM: 24 warps at 80 registers, no spills.
+// Measured on B200 (config 3, ms per K=256 launch): 12x2 0.735, 8x3 0.739,
+// 6x4 0.740, 4x6 0.743, 24x1 0.736, 16x1 (98 registers) 0.924; fewer
+// registers (8x4, 64 registers, spills) 0.80; more (8x2, 108) 0.96.
+constexpr int BATCH_W = 12;
+constexpr int BATCH_MINB = 2;
 template <int MODE>
 static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const double* y,
                                        const double* pq_p, const double* pq_q,
