@@ -218,12 +218,13 @@ struct GlobalJ {
 };
 
 struct StagedJ {
-    double* jst;                  // [p1 - p0] rows g_p, then [q1 - q0] rows g_q
+    double* jp;                   // staged rows g_p[b0..b1): jp[k] is jv[p0 + k]
+    double* jq;                   // staged rows g_q[b0..b1): jq[k] is jv[q0 + k]
     double* __restrict__ jv;
     int32_t p0, p1, q0, q1;
     __device__ __forceinline__ double* loc(int32_t at) const {
-        if (at >= p0 && at < p1) return jst + (at - p0);
-        if (at >= q0 && at < q1) return jst + (p1 - p0) + (at - q0);
+        if (at >= p0 && at < p1) return jp + (at - p0);
+        if (at >= q0 && at < q1) return jq + (at - q0);
         return nullptr;
     }
     __device__ __forceinline__ void put(int32_t at, double v) const {
@@ -601,10 +602,32 @@ __device__ __forceinline__ void single_dev(const GlobalSrc<1>& gs, const DeviceP
 constexpr int SG_SMEM_FOLD = 0;
 constexpr int SG_SMEM_DUP = SG_SMEM_FOLD + 6 * SG_CAP_INC;
 constexpr int SG_SMEM_J = SG_SMEM_DUP + 4 * SG_CAP_DUP;
-constexpr int SG_SMEM_TH = SG_SMEM_J + SG_CAP_J;
+constexpr int SG_SMEM_TH = SG_SMEM_J + SG_CAP_J + 2;   // +2: 16-byte phase shifts
 constexpr int SG_SMEM_V = SG_SMEM_TH + SG_CAP_BUS;
 constexpr int SG_SMEM_DOUBLES = SG_SMEM_V + SG_CAP_BUS;
 constexpr size_t SG_SMEM_BYTES = 8 * (size_t)SG_SMEM_DOUBLES + 4 * (size_t)SG_CAP_BUS;
+
+// Copy n doubles from shared to global memory: the 16-byte aligned middle
+// with one TMA bulk copy (cp.async.bulk), a misaligned head / odd tail with
+// plain stores.  src and dst share their 16-byte phase (see the staging).
+__device__ __forceinline__ void bulk_out(double* dst, const double* src, int32_t n) {
+    int32_t k0 = (int32_t)((reinterpret_cast<uintptr_t>(dst) >> 3) & 1);
+    if (k0 > n) k0 = n;
+    if (k0) dst[0] = src[0];
+    const int32_t pairs = (n - k0) >> 1;
+    if ((n - k0) & 1) dst[n - 1] = src[n - 1];
+    if (pairs > 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t saddr = static_cast<uint32_t>(__cvta_generic_to_shared(src + k0));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     :: "l"(dst + k0), "r"(saddr), "r"(16 * pairs) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
+
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 
 // CTA max -> one integer atomicMax of the |g| bit pattern into the plan's
 // accumulator (exact, order-independent); the last CTA moves it to *norm and
@@ -671,7 +694,15 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
     } else {
         double* fold = sg + SG_SMEM_FOLD;
         double* dupv = sg + SG_SMEM_DUP;
-        double* jst = sg + SG_SMEM_J;
+        // Staged rows keep the 16-byte phase of their global destination, so
+        // the copy-out is one TMA bulk copy per range (plus a lone head /
+        // tail value).  jp / jq start at element 0 or 1 of their slot.
+        const int32_t lp = c1.y - c1.x, lq = c1.w - c1.z;
+        const int32_t sp = (int32_t)((reinterpret_cast<uintptr_t>(jv + c1.x) >> 3) & 1);
+        const int32_t sq0 = sp + lp;
+        const int32_t sq = sq0 + ((sq0 ^ (int32_t)(reinterpret_cast<uintptr_t>(jv + c1.z) >> 3)) & 1);
+        double* jpb = sg + SG_SMEM_J + sp;
+        double* jqb = sg + SG_SMEM_J + sq;
         double* bth = sg + SG_SMEM_TH;
         double* bv = sg + SG_SMEM_V;
         int32_t* bnb = reinterpret_cast<int32_t*>(sg + SG_SMEM_DOUBLES);
@@ -721,10 +752,10 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
                 f[2] = make_double2(v.qt, v.qv);
                 if (r.y & SOLO) {
                     const int32_t w = bnb[o];
-                    jst[r.z] = 0.0 + v.opt;
-                    jst[r.z + w] = 0.0 + v.opv;
-                    jst[r.w] = 0.0 + v.oqt;
-                    jst[r.w + w] = 0.0 + v.oqv;
+                    jpb[r.z] = 0.0 + v.opt;
+                    jpb[r.z + w] = 0.0 + v.opv;
+                    jqb[r.w] = 0.0 + v.oqt;
+                    jqb[r.w + w] = 0.0 + v.oqv;
                 } else {
                     double2* u = reinterpret_cast<double2*>(
                         dupv + 4 * ((r.y >> SG_DUP_SHIFT) & SG_FIELD_MASK));
@@ -741,13 +772,15 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         __syncthreads();
         if (own)   // phase B
             nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1,
-                                        StagedJ{jst, jv, c1.x, c1.y, c1.z, c1.w});
+                                        StagedJ{jpb, jqb, jv, c1.x, c1.y, c1.z, c1.w});
         if (MODE & (JAC | NORM)) __syncthreads();
+        if (MODE & JAC) {   // staged rows out: one TMA bulk copy per range
+            if (t == 0) bulk_out(jv + c1.x, jpb, lp);
+            if (t == 32) bulk_out(jv + c1.z, jqb, lq);
+        }
         if (MODE & NORM) nrm = single_norm(d, nrm, red, norm);
-        if (MODE & JAC) {   // staged rows out as two contiguous ranges
-            const int32_t lp = c1.y - c1.x, lq = c1.w - c1.z;
-            for (int32_t k = t; k < lp; k += SG_THREADS) jv[c1.x + k] = jst[k];
-            for (int32_t k = t; k < lq; k += SG_THREADS) jv[c1.z + k] = jst[lp + k];
+        if (MODE & JAC) {
+            if (t == 0 || t == 32) bulk_wait();   // smem must outlive the copy's reads
         }
         return;
     }

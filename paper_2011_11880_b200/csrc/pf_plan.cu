@@ -662,7 +662,7 @@ int build(const pf_topology* t, pf_plan** out) {
                 const int4 r = hrow[2 * (size_t)own];
                 int32_t f = (own - b0) | (m.z & (SOLO | KSIDE));
                 if (!(m.z & SOLO)) f |= slot++ << SG_DUP_SHIFT;
-                sginc[e] = make_int4(m.x, f, r.x + pos - p0, r.y + pos - q0 + (p1 - p0));
+                sginc[e] = make_int4(m.x, f, r.x + pos - p0, r.y + pos - q0);
             }
             b0 = b1;
         }
