@@ -583,19 +583,34 @@ struct SingleSrc : GlobalSrc<1> {
     }
 };
 
-// load device u's record and operands into registers (types it does not use
-// are left untouched: no out-of-range reads)
-__device__ __forceinline__ void single_dev(const GlobalSrc<1>& gs, const DevicePlan& d, int32_t t,
-                                           bool have, int4& dv, double& a, double& b, double& c,
-                                           double& dd) {
+// Device u's record and operands into registers, in two steps: the record
+// and the plan constants (PQ p0 / q0, PV p0 / v0, Slack v0 / theta0, Shunt
+// g / b) may be read before the programmatic-launch wait; the operands that
+// live in y (PV Q_g, Slack P_s / Q_g) only after it.  Types a device does
+// not use are left untouched: no out-of-range reads.
+__device__ __forceinline__ void single_dev_plan(const GlobalSrc<1>& gs, const DevicePlan& d,
+                                                int32_t t, bool have, int4& dv, double& a,
+                                                double& b, double& c, double& dd) {
     dv = have ? __ldg(d.dev_list + t) : make_int4(-1, 0, 0, 0);
     a = b = c = dd = 0.0;
-    if (dv.x == DEV_PQ || dv.x == DEV_PV || dv.x == DEV_SLACK) {
+    if (dv.x == DEV_PQ) {
         a = gs.dev_a(dv, 0);
         b = gs.dev_b(dv, 0);
+    } else if (dv.x == DEV_PV) {
+        a = gs.dev_a(dv, 0);
     }
     if (dv.x == DEV_PV || dv.x == DEV_SLACK || dv.x == DEV_SHUNT) c = gs.dev_c(dv, 0);
     if (dv.x == DEV_SLACK || dv.x == DEV_SHUNT) dd = gs.dev_d(dv, 0);
+}
+
+__device__ __forceinline__ void single_dev_state(const GlobalSrc<1>& gs, const int4 dv, double& a,
+                                                 double& b) {
+    if (dv.x == DEV_PV) {
+        b = gs.dev_b(dv, 0);
+    } else if (dv.x == DEV_SLACK) {
+        a = gs.dev_a(dv, 0);
+        b = gs.dev_b(dv, 0);
+    }
 }
 
 // shared-memory layout of k_eval_single (doubles, then ints)
@@ -671,6 +686,11 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
     __shared__ double s_tab[PF_TRIG_N * 4];
     const int32_t N = d.N;
     const int t = threadIdx.x;
+    // Programmatic dependent launch (launch_single_mode): the next kernel in
+    // the stream may start while this one runs; it reads only plan data until
+    // its griddepcontrol.wait, after which everything the preceding kernel
+    // wrote (y included, whoever produced it) is visible.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // Every global access is a ~0.5 us round trip here (one wave, one
     // dependent chain per CTA), so loads are issued level by level: chunk
     // record and trig table first, then everything that depends only on
@@ -687,6 +707,7 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
     const Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
     unsigned long long nrm = 0;
     if (c0.y & SG_BIG) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         s_tab[t] = tv0;
         if (t + SG_THREADS < TAB) s_tab[t + SG_THREADS] = tv1;
         __syncthreads();
@@ -708,7 +729,8 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         int32_t* bnb = reinterpret_cast<int32_t*>(sg + SG_SMEM_DOUBLES);
         const int32_t i = b0 + t;
         const bool own = i < b1;
-        // level 2: the first incidence's record and the bus header / state
+        // plan data: the first incidence's record, the bus header, the first
+        // two devices and their constant operands
         const int32_t ea = E0 + t;
         int4 ra = make_int4(0, 0, 0, 0);
         double4 ca = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -721,24 +743,27 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         if (own) {
             src.h0 = __ldg(d.bus_row + 2 * i);
             src.h1 = __ldg(d.bus_row + 2 * i + 1);
-            src.thi = __ldg(y + i);
-            src.vi = __ldg(y + N + i);
+            const int32_t t0 = src.h1.z, nd = src.h1.w - src.h1.z;
+            single_dev_plan(src, d, t0, nd > 0, src.dv0, src.a0, src.b0, src.c0, src.d0);
+            single_dev_plan(src, d, t0 + 1, nd > 1, src.dv1, src.a1, src.b1, src.c1, src.d1);
         }
         s_tab[t] = tv0;
         if (t + SG_THREADS < TAB) s_tab[t + SG_THREADS] = tv1;
-        // level 3: the neighbour's state; devices (record, then operands)
+        // state: after the preceding kernel's writes are visible
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         double tja = 0.0, wja = 0.0;
         if (ea < E1) {
             tja = __ldg(y + ra.x);
             wja = __ldg(y + N + ra.x);
         }
-        if (own) {   // phase 0
+        if (own) {
+            src.thi = __ldg(y + i);
+            src.vi = __ldg(y + N + i);
+            single_dev_state(src, src.dv0, src.a0, src.b0);
+            single_dev_state(src, src.dv1, src.a1, src.b1);
             bth[t] = src.thi;
             bv[t] = src.vi;
             bnb[t] = src.h0.z;
-            const int32_t t0 = src.h1.z, nd = src.h1.w - src.h1.z;
-            single_dev(src, d, t0, nd > 0, src.dv0, src.a0, src.b0, src.c0, src.d0);
-            single_dev(src, d, t0 + 1, nd > 1, src.dv1, src.a1, src.b1, src.c1, src.d1);
         }
         __syncthreads();
         auto incidence = [&](int32_t e, int4 r, double4 c, double tj, double wj) {   // phase A
@@ -987,8 +1012,19 @@ static void launch_single_mode(const DevicePlan& d, const double* y, double* g, 
                              (int)SG_SMEM_BYTES);
         configured = true;
     }
-    k_eval_single<MODE><<<d.sg_chunks, SG_THREADS, SG_SMEM_BYTES, st>>>(
-        d, y, g, j, reinterpret_cast<unsigned long long*>(norm));
+    // programmatic stream serialisation: see k_eval_single
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(d.sg_chunks);
+    cfg.blockDim = dim3(SG_THREADS);
+    cfg.dynamicSmemBytes = SG_SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_eval_single<MODE>, d, y, g, j,
+                       reinterpret_cast<unsigned long long*>(norm));
 }
 
 cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, double* j,

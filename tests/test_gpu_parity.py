@@ -503,3 +503,58 @@ def test_single_grid_chunk_caps_vs_oracle():
         torch.cuda.synchronize()
         assert np.array_equal(gg[: plan.n_var].cpu().numpy(), g)
         assert np.array_equal(jj[: plan.nnz].cpu().numpy(), j)
+
+
+def test_single_grid_back_to_back_and_produced_inputs():
+    """Evaluations queued back to back (programmatic dependent launch lets
+    the next one start early), each on a state that a torch kernel produced
+    just before it, into shared and separate outputs; also inside a CUDA
+    graph.  Every result equals the same evaluation run alone."""
+    s = build_system(synth.config_case(1, seed=1))
+    plan = _plan(s)
+    y0 = _dev(random_state(s, 3))
+    rng = np.random.default_rng(5)
+    deltas = [_dev(rng.normal(0, 0.01, plan.n_var)) for _ in range(6)]
+    ref = []
+    for dl in deltas:
+        g, j, n = _eval(plan, (y0 + dl).cpu().numpy())
+        ref.append((g, j, n))
+
+    def run(out_sep):
+        gs = [plan.empty(plan.n_var) for _ in deltas]
+        js = [plan.empty(plan.nnz) for _ in deltas]
+        ns = plan.empty(len(deltas))
+        ys = [torch.empty_like(y0) for _ in deltas]
+        shared_g, shared_j = plan.empty(plan.n_var), plan.empty(plan.nnz)
+        for k, dl in enumerate(deltas):
+            torch.add(y0, dl, out=ys[k])          # produced right before the evaluation
+            g = gs[k] if out_sep else shared_g
+            j = js[k] if out_sep else shared_j
+            plan.eval(ys[k], g, j, ns[k:k + 1])
+            if not out_sep:
+                gs[k].copy_(shared_g)
+                js[k].copy_(shared_j)
+        return gs, js, ns
+
+    for out_sep in (True, False):
+        gs, js, ns = run(out_sep)
+        torch.cuda.synchronize()
+        for k, (g, j, n) in enumerate(ref):
+            assert np.array_equal(gs[k][: plan.n_var].cpu().numpy(), g)
+            assert np.array_equal(js[k][: plan.nnz].cpu().numpy(), j)
+            assert float(ns[k]) == n
+    # the same sequence captured in a CUDA graph
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        run(True)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        gs, js, ns = run(True)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    for k, (g, j, n) in enumerate(ref):
+        assert np.array_equal(gs[k][: plan.n_var].cpu().numpy(), g)
+        assert np.array_equal(js[k][: plan.nnz].cpu().numpy(), j)
+        assert float(ns[k]) == n
