@@ -176,6 +176,17 @@ PF_API int pf_gather_sum(int32_t n_rows, const int32_t* ptr, const int32_t* idx,
  * test surface like pflow kernels.py:66-72 `sincos`. */
 PF_API int pf_sincos(int64_t n, const double* x, double* s, double* c, void* stream);
 
+/* ---- hand-off to a batched linear solver ----------------
+ * Scenario-major <-> blocked layout.  pf_batch_unblock: dst[s * n_e + e] =
+ * alpha * src(e, s) for s < K (alpha = 1 or -1 is exact), e.g. the CSR
+ * Jacobian values of each scenario as one contiguous array, or -g as the
+ * right-hand sides.  pf_batch_update: y(e, s) += dx[s * n_e + e] for every
+ * scenario with active[s] != 0 (active may be NULL: all).  Device pointers. */
+PF_API int pf_batch_unblock(int32_t K, int32_t n_e, const double* src, double* dst, double alpha,
+                            void* stream);
+PF_API int pf_batch_update(int32_t K, int32_t n_e, double* y, const double* dx,
+                           const int32_t* active, void* stream);
+
 /* Number of kernels this library has launched (process-wide counter). */
 PF_API int64_t pf_launch_count(void);
 

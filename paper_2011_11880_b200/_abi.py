@@ -102,6 +102,8 @@ _SIGS = {
     "pf_join_rows": (C.c_int, [C.c_int32, _VP, _VP, _VP, _VP, _VP, _VP]),
     "pf_gather_sum": (C.c_int, [C.c_int32, _VP, _VP, _VP, _VP, _VP]),
     "pf_sincos": (C.c_int, [C.c_int64, _VP, _VP, _VP, _VP]),
+    "pf_batch_unblock": (C.c_int, [C.c_int32, C.c_int32, _VP, _VP, C.c_double, _VP]),
+    "pf_batch_update": (C.c_int, [C.c_int32, C.c_int32, _VP, _VP, _VP, _VP]),
     "pf_launch_count": (C.c_int64, []),
 }
 

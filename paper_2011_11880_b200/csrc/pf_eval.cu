@@ -995,6 +995,45 @@ __global__ void k_sincos(int64_t n, const double* __restrict__ x, double* __rest
     if (i < n) pf_sincos(x[i], tab, s + i, c + i);
 }
 
+// Blocked <-> scenario-major transposes through a 32 x 33 shared tile:
+// both the 256-byte blocked rows and the scenario-major rows move coalesced.
+// Tile (blockIdx.x: 32 entries, blockIdx.y: scenario block).
+__global__ void k_batch_unblock(int32_t K, int32_t n_e, const double* __restrict__ src,
+                                double* __restrict__ dst, double alpha) {
+    __shared__ double tile[32][33];
+    const int32_t e0 = blockIdx.x * 32, blk = blockIdx.y;
+    const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;   // 8 warps
+    const double* sb = src + (int64_t)blk * n_e * PF_LANES;
+    for (int r = row; r < 32; r += 8) {
+        const int32_t e = e0 + r;
+        tile[r][lane] = e < n_e ? sb[(int64_t)e * PF_LANES + lane] : 0.0;
+    }
+    __syncthreads();
+    for (int r = row; r < 32; r += 8) {
+        const int32_t s = blk * PF_LANES + r, e = e0 + lane;
+        if (s < K && e < n_e) dst[(int64_t)s * n_e + e] = alpha * tile[lane][r];
+    }
+}
+
+__global__ void k_batch_update(int32_t K, int32_t n_e, double* __restrict__ y,
+                               const double* __restrict__ dx, const int32_t* __restrict__ active) {
+    __shared__ double tile[32][33];
+    const int32_t e0 = blockIdx.x * 32, blk = blockIdx.y;
+    const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
+    for (int r = row; r < 32; r += 8) {
+        const int32_t s = blk * PF_LANES + r, e = e0 + lane;
+        tile[r][lane] = (s < K && e < n_e) ? dx[(int64_t)s * n_e + e] : 0.0;
+    }
+    __syncthreads();
+    double* yb = y + (int64_t)blk * n_e * PF_LANES;
+    const int32_t s = blk * PF_LANES + lane;
+    const bool on = s < K && (!active || __ldg(active + s));
+    for (int r = row; r < 32; r += 8) {
+        const int32_t e = e0 + r;
+        if (on && e < n_e) yb[(int64_t)e * PF_LANES + lane] += tile[lane][r];
+    }
+}
+
 inline unsigned grid_for(int64_t n, int threads) {
     return (unsigned)((n + threads - 1) / threads);
 }
@@ -1170,6 +1209,24 @@ cudaError_t launch_gather_sum(int32_t n, const int32_t* ptr, const int32_t* idx,
                               const double* vals, double* out, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     k_gather_sum<<<grid_for(n, 256), 256, 0, st>>>(n, ptr, idx, vals, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batch_unblock(int32_t K, int32_t n_e, const double* src, double* dst,
+                                 double alpha, cudaStream_t st) {
+    if (K <= 0 || n_e <= 0) return cudaSuccess;
+    const dim3 grid(grid_for(n_e, 32), (unsigned)((K + PF_LANES - 1) / PF_LANES));
+    k_batch_unblock<<<grid, 256, 0, st>>>(K, n_e, src, dst, alpha);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batch_update(int32_t K, int32_t n_e, double* y, const double* dx,
+                                const int32_t* active, cudaStream_t st) {
+    if (K <= 0 || n_e <= 0) return cudaSuccess;
+    const dim3 grid(grid_for(n_e, 32), (unsigned)((K + PF_LANES - 1) / PF_LANES));
+    k_batch_update<<<grid, 256, 0, st>>>(K, n_e, y, dx, active);
     count_launch();
     return cudaGetLastError();
 }

@@ -147,6 +147,10 @@ cudaError_t launch_join_rows(int32_t n, const int32_t* ptr, const int32_t* split
                              const int32_t* idx, const double* pool, double* out,
                              cudaStream_t st);
 cudaError_t launch_sincos(int64_t n, const double* x, double* s, double* c, cudaStream_t st);
+cudaError_t launch_batch_unblock(int32_t K, int32_t n_e, const double* src, double* dst,
+                                 double alpha, cudaStream_t st);
+cudaError_t launch_batch_update(int32_t K, int32_t n_e, double* y, const double* dx,
+                                const int32_t* active, cudaStream_t st);
 cudaError_t launch_gather_sum(int32_t n, const int32_t* ptr, const int32_t* idx,
                               const double* vals, double* out, cudaStream_t st);
 

@@ -787,6 +787,22 @@ int pf_eval_batched(const pf_plan* p, int32_t K, const double* y, const double* 
     return PF_OK;
 }
 
+int pf_batch_unblock(int32_t K, int32_t n_e, const double* src, double* dst, double alpha,
+                     void* stream) {
+    if (K < 0 || n_e < 0) return pf::invalid("negative size");
+    if ((K > 0 && n_e > 0) && (!src || !dst)) return pf::invalid("NULL argument");
+    PF_CUDA(pf::launch_batch_unblock(K, n_e, src, dst, alpha, (cudaStream_t)stream));
+    return PF_OK;
+}
+
+int pf_batch_update(int32_t K, int32_t n_e, double* y, const double* dx, const int32_t* active,
+                    void* stream) {
+    if (K < 0 || n_e < 0) return pf::invalid("negative size");
+    if ((K > 0 && n_e > 0) && (!y || !dx)) return pf::invalid("NULL argument");
+    PF_CUDA(pf::launch_batch_update(K, n_e, y, dx, active, (cudaStream_t)stream));
+    return PF_OK;
+}
+
 int pf_jac_to_csc(const pf_plan* p, int32_t K, const double* jcsr, double* jcsc, void* stream) {
     if (!p || !jcsr || !jcsc) return pf::invalid("NULL argument");
     PF_CUDA(pf::launch_jac_to_csc(p->d, K, jcsr, jcsc, (cudaStream_t)stream));

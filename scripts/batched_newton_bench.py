@@ -1,0 +1,86 @@
+"""Batched Newton on the device vs pflow's loop on the CPU.
+
+Workload: a config-0-shaped synthetic grid (2,000 buses, 2,500 branches) with
+loads scaled to 5 % so that Newton converges from a flat start; K scenarios
+from ``synth.make_scenarios`` (load / PV scaling, one outage each).
+
+* GPU: ``batched_newton_solve``. Evaluation runs through pf_eval_batched;
+  each scenario's refactorisation and solve run through cusolverRf.
+* CPU: pflow/newton.py's loop restated on the C oracle (wf1 g and J) with
+  SuperLU, one scenario after another, on one core.
+
+Prints one JSON line: both times, per-phase GPU timings, and the agreement
+(outcomes, iteration counts, max |y_gpu - y_cpu|).
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+
+def main():
+    import torch
+
+    import oracle
+    from test_gpu_parity import _cpu_newton, _light_case
+    from paper_2011_11880_b200 import synth
+    from paper_2011_11880_b200.batched_newton import batched_newton_solve
+    from paper_2011_11880_b200.plan import Plan, from_blocked, to_blocked
+    from paper_2011_11880_b200.system_model import build_system, flat_start
+
+    K = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    s = build_system(_light_case(2000, 2500, seed=0))
+    plan = Plan(s)
+    o = oracle.Oracle(s)
+    sb = synth.make_scenarios(s, K, seed=1)
+    y0 = flat_start(s)
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+    t = lambda a: dev(to_blocked(np.ascontiguousarray(a.T)))
+    args = (t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), torch.as_tensor(sb.outage, device="cuda"))
+    # warm-up (library load, kernels)
+    yw = dev(to_blocked(np.tile(y0, (K, 1))))
+    batched_newton_solve(plan, K, yw, *args)
+    y = dev(to_blocked(np.tile(y0, (K, 1))))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = batched_newton_solve(plan, K, y, *args)
+    torch.cuda.synchronize()
+    gpu_s = time.perf_counter() - t0
+    Y = from_blocked(y.cpu().numpy(), K, plan.n_var)
+
+    t0 = time.perf_counter()
+    cpu = [_cpu_newton(o, y0, sb.pq_p[:, k].copy(), sb.pq_q[:, k].copy(), sb.pv_p[:, k].copy(),
+                       int(sb.outage[k])) for k in range(K)]
+    cpu_s = time.perf_counter() - t0
+    agree = sum(int((st == "converged") == bool(res.converged[k])) for k, (st, _, _) in enumerate(cpu))
+    same_it = sum(int(st == "converged" and res.converged[k] and res.iterations[k] == it)
+                  for k, (st, it, _) in enumerate(cpu))
+    conv = [k for k, (st, _, _) in enumerate(cpu) if st == "converged" and res.converged[k]]
+    dmax = max((float(np.abs(Y[k] - cpu[k][2]).max()) for k in conv), default=None)
+    line = {
+        "workload": f"2,000-bus synthetic grid (loads x0.05), K={K} scenarios, Newton from flat "
+                    "start, tol 1e-8",
+        "n_var": plan.n_var, "nnz": plan.nnz,
+        "gpu_s": gpu_s, "gpu_timings_s": res.timings,
+        "gpu_scenarios_per_s": K / gpu_s,
+        "cpu_s": cpu_s, "cpu_scenarios_per_s": K / cpu_s, "cpu_cores": 1,
+        "converged_gpu": int(res.converged.sum()), "singular_gpu": int(res.singular.sum()),
+        "converged_cpu": sum(int(st == "converged") for st, _, _ in cpu),
+        "outcome_agreement": agree, "same_iterations": same_it,
+        "max_abs_state_diff": dmax,
+        "iterations": int(res.iterations.max()),
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -558,3 +558,79 @@ def test_single_grid_back_to_back_and_produced_inputs():
         assert np.array_equal(gs[k][: plan.n_var].cpu().numpy(), g)
         assert np.array_equal(js[k][: plan.nnz].cpu().numpy(), j)
         assert float(ns[k]) == n
+
+
+def _light_case(n_bus, n_branch, seed, scale=0.05):
+    raw = synth.synth_case(n_bus, n_branch, seed=seed, pq_frac=0.6, pv_frac=0.15,
+                           shunt_frac=0.1, name=f"light{n_bus}")
+    for col in ("pd", "qd", "pg"):
+        getattr(raw, col)[:] *= scale
+    return raw
+
+
+def _cpu_newton(o, y, pq_p, pq_q, pv_p, outage, tol=1e-8, max_iter=20):
+    """pflow/newton.py:49-112 for one scenario: oracle g/J + SuperLU."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    n = o.n_var
+    cptr, cidx = o.pattern_csc()
+    y = y.copy()
+    it = 0
+    while True:
+        g, j, nrm = o.eval_scenarios(1, to_blocked(y[None, :]), to_blocked(pq_p[None, :]),
+                                     to_blocked(pq_q[None, :]), to_blocked(pv_p[None, :]),
+                                     np.array([outage], np.int32))
+        g = from_blocked(g, 1, n)[0]
+        m = float(nrm[0])
+        if not np.isfinite(m) or m > 1e6:
+            return "diverged", it, y
+        if m <= tol:
+            return "converged", it, y
+        if it >= max_iter:
+            return "max_iter", it, y
+        jv = from_blocked(j, 1, o.nnz)[0]
+        try:
+            dy = spla.splu(sp.csc_matrix((jv, cidx, cptr), shape=(n, n))).solve(-g)
+        except RuntimeError:
+            return "singular", it, y
+        y += dy
+        it += 1
+
+
+def test_batched_newton_vs_cpu_newton():
+    """Device-resident batched Newton (pf_eval_batched + cusolverRf
+    refactorisation on the fixed pattern) against pflow's loop restated on the
+    CPU oracle with SuperLU, scenario by scenario: same outcome, same
+    iteration count, same converged state."""
+    from paper_2011_11880_b200.batched_newton import batched_newton_solve
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+    from paper_2011_11880_b200.system_model import flat_start
+
+    s = build_system(_light_case(300, 390, seed=3))
+    plan = _plan(s)
+    o = oracle.Oracle(s)
+    K = 24
+    sb = synth.make_scenarios(s, K, seed=4)
+    y0 = flat_start(s)
+    Y = np.tile(y0, (K, 1))
+    y_dev = _dev(to_blocked(Y))
+    t = lambda a: _dev(to_blocked(np.ascontiguousarray(a.T)))
+    outage = torch.as_tensor(sb.outage, device="cuda")
+    res = batched_newton_solve(plan, K, y_dev, t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), outage)
+    Yg = from_blocked(y_dev.cpu().numpy(), K, plan.n_var)
+    n_conv = 0
+    for k in range(K):
+        status, it, yk = _cpu_newton(o, y0, sb.pq_p[:, k].copy(), sb.pq_q[:, k].copy(),
+                                     sb.pv_p[:, k].copy(), int(sb.outage[k]))
+        if status == "converged":
+            n_conv += 1
+            assert res.converged[k], k
+            assert res.iterations[k] == it, (k, res.iterations[k], it)
+            np.testing.assert_allclose(Yg[k], yk, rtol=0, atol=1e-9)
+            assert res.final_mismatch[k] <= 1e-8
+        else:
+            assert not res.converged[k], (k, status)
+    assert n_conv >= K // 2
