@@ -41,6 +41,10 @@ def __getattr__(name):
         from . import newton
 
         return getattr(newton, name)
+    if name in ("BatchedLU", "BatchedResult", "batched_newton_solve"):
+        from . import batched_newton
+
+        return getattr(batched_newton, name)
     if name in ("ScenarioBuffers", "gather_norms", "shard"):
         from . import batched
 
@@ -49,10 +53,10 @@ def __getattr__(name):
 
 
 __all__ = [
-    "AddressMap", "CaseFormatError", "JacobianWorkspace", "LineGroup", "NewtonOptions", "Plan",
+    "AddressMap", "BatchedLU", "BatchedResult", "CaseFormatError", "JacobianWorkspace", "LineGroup", "NewtonOptions", "Plan",
     "PowerSystem", "PqGroup", "PvGroup", "RawCase", "ResidualWorkspace", "ScenarioBuffers",
     "ShuntGroup", "SlackGroup", "SolveResult", "Violation", "build_system", "count_variables",
-    "evaluate_jacobian", "evaluate_residual", "finite_difference_jacobian", "flat_start",
+    "batched_newton_solve", "evaluate_jacobian", "evaluate_residual", "finite_difference_jacobian", "flat_start",
     "from_rows", "gather_norms", "make_case", "newton_solve", "parse_case", "parse_case_file",
     "random_state", "shard", "symbolic_pattern", "validate_case", "write_case",
 ]

@@ -634,3 +634,32 @@ def test_batched_newton_vs_cpu_newton():
         else:
             assert not res.converged[k], (k, status)
     assert n_conv >= K // 2
+
+
+def test_batch_unblock_and_update_kernels():
+    """pf_batch_unblock / pf_batch_update against numpy (K not a multiple of
+    32, n_e not a multiple of 32, an inactive scenario left untouched)."""
+    from paper_2011_11880_b200 import _abi
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    rng = np.random.default_rng(9)
+    K, n_e = 45, 1037
+    X = rng.normal(size=(K, n_e))
+    src = _dev(to_blocked(X))
+    dst = torch.empty((K, n_e), dtype=torch.float64, device="cuda")
+    _abi.check(_abi.lib().pf_batch_unblock(K, n_e, src.data_ptr(), dst.data_ptr(), -1.0, None))
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.cpu().numpy(), -X)
+    dx = rng.normal(size=(K, n_e))
+    active = np.ones(K, np.int32)
+    active[[3, 40]] = 0
+    y = _dev(to_blocked(X))
+    d_dx = _dev(dx)                                   # keep the buffers alive over the launch
+    d_act = torch.as_tensor(active, device="cuda")
+    _abi.check(_abi.lib().pf_batch_update(K, n_e, y.data_ptr(), d_dx.data_ptr(), d_act.data_ptr(),
+                                          None))
+    torch.cuda.synchronize()
+    Y = from_blocked(y.cpu().numpy(), K, n_e)
+    want = X + dx * active[:, None]
+    want[[3, 40]] = X[[3, 40]]
+    assert np.array_equal(Y, want)
