@@ -532,9 +532,11 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
 //   B: each bus thread folds its incidences in list order (the reference's
 //      join and assembly association), adds the parallel-branch values in
 //      order and its devices, and writes g and its diagonal / device values;
-// then the CTA copies its staged rows g_p[b0..b1), g_q[b0..b1) out as two
-// contiguous, coalesced ranges.  A chunk whose single bus exceeds the caps
-// (a hub) is evaluated serially by one thread from global memory.
+// then the CTA copies its staged rows g_p[b0..b1), g_q[b0..b1) out with two
+// TMA bulk copies.  A chunk whose single bus exceeds the caps (a hub) is
+// evaluated serially by one thread from global memory.  Launched with
+// programmatic stream serialisation (launch_single_mode): plan data is read
+// before griddepcontrol.wait, the state and every output after it.
 struct SingleSrc : GlobalSrc<1> {
     static constexpr bool kSplit = true;
     const double* fold;                // [n_inc of chunk][6] {fp, fq, pt, pv, qt, qv}
