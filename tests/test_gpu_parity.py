@@ -275,6 +275,12 @@ def test_stress_hubs_config4_shape():
     fails = sum(parity_failures(G[k], g_ref[k]) + parity_failures(J[k][perm], j_ref[k])
                 for k in range(K))
     assert fails == 0
+    # the single-grid kernel on the same hub topology (chunks hold the hubs)
+    y = random_state(s, 77)
+    g, j, norm = _eval(plan, y)
+    assert_parity(g, o.residual(y), "hub grid single g")
+    assert_parity(j[perm], o.jacobian(y), "hub grid single J")
+    assert norm == np.abs(g).max()
 
 
 def test_host_batched_pipeline_matches_device():
