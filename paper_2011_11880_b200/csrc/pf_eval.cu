@@ -733,13 +733,16 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         const bool own = i < b1;
         // plan data: the first incidence's record, the bus header, the first
         // two devices and their constant operands
-        const int32_t ea = E0 + t;
-        int4 ra = make_int4(0, 0, 0, 0);
+        // (chunks hold at most 2 SG_THREADS incidences: two per thread)
+        static_assert(SG_CAP_INC <= 2 * SG_THREADS, "two incidences per thread");
+        const int32_t ea = E0 + t, eb = ea + SG_THREADS;
+        int4 ra = make_int4(0, 0, 0, 0), rb = make_int4(0, 0, 0, 0);
         double4 ca = make_double4(0.0, 0.0, 0.0, 0.0);
         if (ea < E1) {
             ra = __ldg(d.sg_inc + ea);
             ca = ldg4(d.inc_coef + ea);
         }
+        if (eb < E1) rb = __ldg(d.sg_inc + eb);
         SingleSrc src{{d, A, y, i, 0}, fold, dupv, E0, make_int4(0, 0, 0, 0),
                       make_int4(0, 0, 0, 0), 0.0, 0.0};
         if (own) {
@@ -753,10 +756,14 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         if (t + SG_THREADS < TAB) s_tab[t + SG_THREADS] = tv1;
         // state: after the preceding kernel's writes are visible
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        double tja = 0.0, wja = 0.0;
+        double tja = 0.0, wja = 0.0, tjb = 0.0, wjb = 0.0;
         if (ea < E1) {
             tja = __ldg(y + ra.x);
             wja = __ldg(y + N + ra.x);
+        }
+        if (eb < E1) {
+            tjb = __ldg(y + rb.x);
+            wjb = __ldg(y + N + rb.x);
         }
         if (own) {
             src.thi = __ldg(y + i);
@@ -792,10 +799,7 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             }
         };
         if (ea < E1) incidence(ea, ra, ca, tja, wja);
-        for (int32_t e = ea + SG_THREADS; e < E1; e += SG_THREADS) {
-            const int4 r = __ldg(d.sg_inc + e);
-            incidence(e, r, ldg4(d.inc_coef + e), __ldg(y + r.x), __ldg(y + N + r.x));
-        }
+        if (eb < E1) incidence(eb, rb, ldg4(d.inc_coef + eb), tjb, wjb);
         __syncthreads();
         if (own)   // phase B
             nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1,
