@@ -17,6 +17,8 @@ from .case import (CaseFormatError, RawCase, Violation, from_rows, make_case, pa
                    parse_case_file, validate_case, write_case)
 from .system_model import (AddressMap, LineGroup, PowerSystem, PqGroup, PvGroup, ShuntGroup,
                            SlackGroup, build_system, count_variables, flat_start, random_state)
+from .workflow import (WORKFLOW_TABLE, IntraStrategy, WorkflowConfig, WorkflowConfigError,
+                       all_workflows, set_worker_count, worker_count, workflow_config)
 
 __version__ = "0.1.0"
 
@@ -37,7 +39,8 @@ def __getattr__(name):
         from . import jacobian
 
         return getattr(jacobian, name)
-    if name in ("NewtonOptions", "SolveResult", "newton_solve"):
+    if name in ("NewtonOptions", "SolveResult", "newton_solve", "SingularMatrixError",
+                "SuperLUSolver"):
         from . import newton
 
         return getattr(newton, name)
@@ -59,4 +62,6 @@ __all__ = [
     "batched_newton_solve", "evaluate_jacobian", "evaluate_residual", "finite_difference_jacobian", "flat_start",
     "from_rows", "gather_norms", "make_case", "newton_solve", "parse_case", "parse_case_file",
     "random_state", "shard", "symbolic_pattern", "validate_case", "write_case",
+    "SingularMatrixError", "SuperLUSolver", "WORKFLOW_TABLE", "IntraStrategy", "WorkflowConfig",
+    "WorkflowConfigError", "all_workflows", "set_worker_count", "worker_count", "workflow_config",
 ]

@@ -1,16 +1,17 @@
 """Newton-Raphson driver around the GPU evaluation.
 
-Restates pflow/newton.py:49-112 - the full-step NR loop, the infinity-norm
-convergence test and the 1e6 / non-finite divergence guard - with the
-residual, Jacobian and norm evaluated by libpfgpu.  The state, g and J stay on
-the device; the linear solve (task 3, outside the product per BASELINE.json)
-is delegated to a caller-supplied solver on the CSC matrix, by default
-``scipy.sparse.linalg.splu``.
+Restates pflow/newton.py:49-112 with the same signature, options, result and
+error behaviour. The loop is a full-step Newton. It stops on the
+infinity-norm mismatch, and its divergence guard is 1e6 or non-finite. A
+singular Jacobian raises ``SingularMatrixError``; non-convergence is an
+outcome, not an error. The residual, the Jacobian and the norm are evaluated
+by libpfgpu, and g and J stay on the device. Each iteration reads back one
+scalar, the norm, plus g and the CSC values when a linear solve follows.
 
-It also accepts the reference's own duck-typed workspaces contract: the
-workspaces in ``residual.py`` / ``jacobian.py`` can be passed to pflow's
-``newton_solve`` directly; this module is the device-resident
-variant that avoids a host round trip of g for the norm.
+The linear solve (task 3) is outside the product (BASELINE.json). It goes to
+``solver``, given either pflow's way (an object with ``.solve(a_csc, b)``,
+such as pflow's own ``BuiltinLU``) or as a plain ``(a_csc, b) -> dy``
+callable. The default is SuperLU (``scipy.sparse.linalg.splu``).
 """
 
 from __future__ import annotations
@@ -23,14 +24,21 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from .plan import Plan
+from .workflow import WorkflowConfig, workflow_config
 
 _DIVERGENCE_LIMIT = 1e6   # pflow/newton.py:23
+
+
+class SingularMatrixError(RuntimeError):
+    """The Jacobian is singular (pflow/linear_solver.py:28)."""
 
 
 @dataclass(frozen=True)
 class NewtonOptions:
     tol: float = 1e-8
     max_iter: int = 20
+    # accepted for pflow compatibility; the GPU path has one execution strategy
+    workflow: WorkflowConfig = field(default_factory=lambda: workflow_config(1))
 
     def __post_init__(self):
         if self.tol <= 0:
@@ -49,17 +57,37 @@ class SolveResult:
     diverged: bool = False
 
 
+class SuperLUSolver:
+    """Default linear solver: ``.solve(a_csc, b)`` with SuperLU."""
+
+    def solve(self, a: sp.csc_matrix, b: np.ndarray) -> np.ndarray:
+        try:
+            return spla.splu(a).solve(b)
+        except RuntimeError as e:          # "Factor is exactly singular"
+            raise SingularMatrixError(str(e)) from None
+
+
 def splu_solver(csc: sp.csc_matrix, rhs: np.ndarray) -> np.ndarray:
-    return spla.splu(csc).solve(rhs)
+    return SuperLUSolver().solve(csc, rhs)
 
 
-def newton_solve(sys, y0, opts: NewtonOptions | None = None, plan: Plan | None = None,
-                 solver=splu_solver) -> SolveResult:
-    """Iterate y <- y + dy with J dy = -g until max|g| <= tol (pflow/newton.py:49-112)."""
+def _solve(solver, a, b):
+    return solver.solve(a, b) if hasattr(solver, "solve") else solver(a, b)
+
+
+def newton_solve(sys, y0, opts: NewtonOptions | None = None, solver=None, residual_ws=None,
+                 jacobian_ws=None, *, plan: Plan | None = None) -> SolveResult:
+    """Iterate y <- y + dy with J dy = -g until max|g| <= tol
+    (pflow/newton.py:49-112).  ``residual_ws`` / ``jacobian_ws`` may be this
+    package's workspaces: their plan is reused."""
     import torch
 
     opts = opts or NewtonOptions()
+    for ws in (residual_ws, jacobian_ws):
+        if plan is None and ws is not None and isinstance(getattr(ws, "plan", None), Plan):
+            plan = ws.plan
     plan = plan if plan is not None else Plan(sys)
+    solver = solver if solver is not None else SuperLUSolver()
     y0 = np.asarray(y0, dtype=np.float64)
     if y0.shape != (plan.n_var,):
         raise ValueError(f"y0 has shape {y0.shape}, expected ({plan.n_var},)")
@@ -79,7 +107,7 @@ def newton_solve(sys, y0, opts: NewtonOptions | None = None, plan: Plan | None =
     while True:
         t0 = time.perf_counter()
         plan.eval(y, g=g, norm=norm)          # residual + fused infinity norm
-        mismatch = float(norm[0])             # the one scalar read back per iteration
+        mismatch = float(norm[0]) if n else 0.0   # the one scalar read back per iteration
         timings["residual"] += time.perf_counter() - t0
         if (not np.isfinite(mismatch) or mismatch > _DIVERGENCE_LIMIT
                 or not bool(torch.isfinite(y).all())):
@@ -97,7 +125,7 @@ def newton_solve(sys, y0, opts: NewtonOptions | None = None, plan: Plan | None =
         rhs = -g[:n].cpu().numpy()
         timings["jacobian"] += time.perf_counter() - t0
         t0 = time.perf_counter()
-        dy = solver(csc, rhs)
+        dy = _solve(solver, csc, rhs)
         timings["linear"] += time.perf_counter() - t0
         t0 = time.perf_counter()
         y += torch.as_tensor(dy, device=plan.device)

@@ -669,3 +669,51 @@ def test_batch_unblock_and_update_kernels():
     want = X + dx * active[:, None]
     want[[3, 40]] = X[[3, 40]]
     assert np.array_equal(Y, want)
+
+
+@pytest.mark.parametrize("name", ["tiny_edge", "edge300", "config0"])
+def test_newton_driver_failure_modes_match_reference(name):
+    """Where pflow's own solve fails, the GPU-driven one fails the same way:
+    SingularMatrixError for the fixtures with isolated buses (pflow raised
+    there), the same non-converged iteration count otherwise."""
+    from paper_2011_11880_b200.newton import NewtonOptions, SingularMatrixError, newton_solve
+    from paper_2011_11880_b200.system_model import flat_start
+
+    d = load(name)
+    s = system_of(d)
+    assert not bool(d["newton_converged"])
+    if "newton_iterations" not in d.files:
+        with pytest.raises(SingularMatrixError):
+            newton_solve(s, flat_start(s), NewtonOptions())
+    else:
+        res = newton_solve(s, flat_start(s), NewtonOptions())
+        assert not res.converged
+        assert res.iterations == int(d["newton_iterations"])
+
+
+def test_newton_driver_takes_pflow_style_solver_and_workspaces():
+    """pflow's calling convention: newton_solve(sys, y0, opts, solver,
+    residual_ws=, jacobian_ws=) with a solver object exposing .solve(a, b)."""
+    import scipy.sparse.linalg as spla
+
+    from paper_2011_11880_b200.jacobian import JacobianWorkspace
+    from paper_2011_11880_b200.newton import NewtonOptions, newton_solve
+    from paper_2011_11880_b200.residual import ResidualWorkspace
+    from paper_2011_11880_b200.system_model import flat_start
+    from paper_2011_11880_b200.workflow import workflow_config
+
+    class Solver:
+        calls = 0
+
+        def solve(self, a, b):
+            Solver.calls += 1
+            return spla.spsolve(a, b)
+
+    d = load("case14")
+    s = system_of(d)
+    plan = _plan(s)
+    res = newton_solve(s, flat_start(s), NewtonOptions(workflow=workflow_config(5)), Solver(),
+                       residual_ws=ResidualWorkspace(s, plan), jacobian_ws=JacobianWorkspace(s, plan))
+    assert res.converged and res.iterations == int(d["newton_iterations"])
+    assert Solver.calls == res.iterations
+    assert np.abs(res.y - d["newton_y"]).max() < 1e-8
