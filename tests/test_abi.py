@@ -74,3 +74,20 @@ def test_plan_create_rejects_bad_topology_before_touching_gpu(built):
     assert rc == _abi.PF_EINVAL
     assert b"bus index" in _abi.lib().pf_last_error()
     del keep
+
+
+def test_host_side_argument_checks_without_gpu(built):
+    """NULL / negative arguments are rejected on the host with PF_EINVAL and a
+    message, before any CUDA call (pflow raises ValueError at bind time)."""
+    lib = _abi.lib()
+    assert lib.pf_batch_unblock(-1, 4, None, None, 1.0, None) == _abi.PF_EINVAL
+    assert b"negative" in lib.pf_last_error()
+    assert lib.pf_batch_unblock(2, 4, None, None, 1.0, None) == _abi.PF_EINVAL
+    assert b"NULL" in lib.pf_last_error()
+    assert lib.pf_batch_update(2, 4, None, None, None, None) == _abi.PF_EINVAL
+    assert lib.pf_eval(None, None, None, None, None, None) == _abi.PF_EINVAL
+    assert lib.pf_plan_destroy(None) in (_abi.PF_OK, _abi.PF_EINVAL)
+    with pytest.raises(ValueError):
+        _abi.check(_abi.PF_EINVAL)
+    with pytest.raises(RuntimeError):
+        _abi.check(_abi.PF_ECUDA)
