@@ -47,7 +47,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from . import _abi
-from .plan import PF_LANES, Plan
+from .plan import Plan
 
 _DIVERGENCE_LIMIT = 1e6   # pflow/newton.py:23
 
@@ -94,13 +94,6 @@ def _rf():
             "cusolverRfSetMatrixFormat": [vp, i32, i32],
             "cusolverRfSetAlgs": [vp, i32, i32],
             "cusolverRfSetNumericProperties": [vp, f64, f64],
-            "cusolverRfBatchSetupHost": [i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, i32, vp, vp,
-                                         vp, vp, vp, vp],
-            "cusolverRfBatchAnalyze": [vp],
-            "cusolverRfBatchResetValues": [i32, i32, i32, vp, vp, vp, vp, vp, vp],
-            "cusolverRfBatchRefactor": [vp],
-            "cusolverRfBatchSolve": [vp, vp, vp, i32, vp, i32, vp, i32],
-            "cusolverRfBatchZeroPivot": [vp, vp],
             "cusolverRfSetupHost": [i32, i32, vp, vp, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp,
                                     vp],
             "cusolverRfAnalyze": [vp],
