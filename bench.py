@@ -332,7 +332,7 @@ def run_gpu(args):
         dist.barrier()
 
     if rank == 0 and world == 1 and not args.no_single and args.workload == "config3":
-        line["single_grid"] = single_grid(dev, steps=max(20, args.steps))
+        line["single_grid"] = single_grid(dev, steps=max(20, args.steps), cpu=not args.no_cpu)
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         r = cpu_reference(sys_, K, 2000, 1, 1, threads, min_seconds=args.cpu_seconds)
@@ -347,7 +347,7 @@ def run_gpu(args):
     return 0
 
 
-def single_grid(dev, steps: int) -> dict:
+def single_grid(dev, steps: int, cpu: bool = True) -> dict:
     """Single grids, one f+J+norm per evaluation (BASELINE configs 0-2).
 
     cold: L2 flushed (256 MB write) before every evaluation, CUDA events
@@ -357,12 +357,41 @@ def single_grid(dev, steps: int) -> dict:
     The top-level keys are config 2 (the metric's 70k-bus grid); configs 0
     and 1 are listed under "smaller".
     """
-    out = _single_grid_config(dev, 2, steps)
-    out["smaller"] = [_single_grid_config(dev, c, steps) for c in (0, 1)]
+    out = _single_grid_config(dev, 2, steps, cpu)
+    out["smaller"] = [_single_grid_config(dev, c, steps, cpu) for c in (0, 1)]
     return out
 
 
-def _single_grid_config(dev, cfg: int, steps: int) -> dict:
+def single_cpu_baseline(sys_, y, min_seconds: float = 0.5) -> dict:
+    """The reference's fastest CPU workflow for one grid:
+    pflow's f+J restated in C (oracle/), wf1 and wf5 on one thread and wf3 on
+    every host thread; the fastest one's median over >= min_seconds."""
+    import oracle  # cpu_baseline leg only
+
+    o = oracle.Oracle(sys_)
+    threads = os.cpu_count() or 1
+    runs = {1: lambda: (o.residual(y, 1), o.jacobian(y, 1)),
+            5: lambda: (o.residual(y, 5), o.jacobian(y, 5)),
+            3: lambda: o.eval_threaded(y, threads)}
+    best = None
+    for wf, fn in runs.items():
+        fn()
+        times, t_start = [], time.perf_counter()
+        while len(times) < 3 or time.perf_counter() - t_start < min_seconds:
+            t0 = time.perf_counter()
+            fn()
+            times.append(time.perf_counter() - t0)
+        med = statistics.median(times)
+        if best is None or med < best[1]:
+            best = (wf, med)
+    wf, med = best
+    return {"value": 1.0 / med, "unit": "evals/s", "us_per_eval": med * 1e6,
+            "cores": threads if wf == 3 else 1, "kind": "port", "wf": wf,
+            "sample": "fastest of pflow wf1 / wf5 (one thread) and wf3 (all host threads), "
+                      "restated in C (oracle/), median per f+J"}
+
+
+def _single_grid_config(dev, cfg: int, steps: int, cpu: bool = True) -> dict:
     import torch
 
     from paper_2011_11880_b200 import synth
@@ -419,7 +448,8 @@ def _single_grid_config(dev, cfg: int, steps: int) -> dict:
             "cold_frac": bytes_eval / (med_c / 1e3) / 1e9 / peak,
             "graph100_frac": bytes_eval / (med_g / 1e3) / 1e9 / peak,
             "n_var": plan.n_var, "nnz": plan.nnz, "kernel": "k_eval_single<RES|JAC|NORM>",
-            "ctas": plan.single_chunks}
+            "ctas": plan.single_chunks,
+            "cpu_baseline": single_cpu_baseline(s, y0) if cpu else None}
 
 
 def main():
