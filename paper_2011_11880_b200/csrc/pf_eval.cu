@@ -1049,8 +1049,8 @@ inline unsigned grid_for(int64_t n, int threads) {
 // ---- launchers --------------------------------------------------------------
 
 template <int MODE>
-static void launch_single_mode(const DevicePlan& d, const double* y, double* g, double* j,
-                               double* norm, cudaStream_t st) {
+static cudaError_t launch_single_mode(const DevicePlan& d, const double* y, double* g, double* j,
+                                      double* norm, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_eval_single<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1068,8 +1068,8 @@ static void launch_single_mode(const DevicePlan& d, const double* y, double* g, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_eval_single<MODE>, d, y, g, j,
-                       reinterpret_cast<unsigned long long*>(norm));
+    return cudaLaunchKernelEx(&cfg, k_eval_single<MODE>, d, y, g, j,
+                              reinterpret_cast<unsigned long long*>(norm));
 }
 
 cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, double* j,
@@ -1079,16 +1079,20 @@ cudaError_t launch_eval_single(const DevicePlan& d, const double* y, double* g, 
         return cudaSuccess;
     }
     const int mode = (g ? RES : 0) | (j ? JAC : 0) | (norm ? NORM : 0);
+#define PF_S(M) launch_single_mode<M>(d, y, g, j, norm, st)
+    cudaError_t e = cudaSuccess;
     switch (mode) {
-        case RES: launch_single_mode<RES>(d, y, g, j, norm, st); break;
-        case JAC: launch_single_mode<JAC>(d, y, g, j, norm, st); break;
-        case RES | JAC: launch_single_mode<RES | JAC>(d, y, g, j, norm, st); break;
-        case NORM: launch_single_mode<NORM>(d, y, g, j, norm, st); break;
-        case RES | NORM: launch_single_mode<RES | NORM>(d, y, g, j, norm, st); break;
-        case JAC | NORM: launch_single_mode<JAC | NORM>(d, y, g, j, norm, st); break;
-        case RES | JAC | NORM: launch_single_mode<RES | JAC | NORM>(d, y, g, j, norm, st); break;
+        case RES: e = PF_S(RES); break;
+        case JAC: e = PF_S(JAC); break;
+        case RES | JAC: e = PF_S(RES | JAC); break;
+        case NORM: e = PF_S(NORM); break;
+        case RES | NORM: e = PF_S(RES | NORM); break;
+        case JAC | NORM: e = PF_S(JAC | NORM); break;
+        case RES | JAC | NORM: e = PF_S(RES | JAC | NORM); break;
         default: return cudaSuccess;
     }
+#undef PF_S
+    if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
 }
