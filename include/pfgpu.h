@@ -187,6 +187,46 @@ PF_API int pf_batch_unblock(int32_t K, int32_t n_e, const double* src, double* d
 PF_API int pf_batch_update(int32_t K, int32_t n_e, double* y, const double* dx,
                            const int32_t* active, void* stream);
 
+/* ---- batched sparse LU on a fixed schedule -------------
+ * The K scenarios share one pattern, pivot order and elimination schedule
+ * (built on the host by paper_2011_11880_b200/batched_lu.py); factor values
+ * M (nnz_m per scenario) and vectors (n per scenario) use the blocked layout.
+ *   pf_lu_scatter     M = 0, then M[a2m[e]] = A[e]                     (A: CSR values)
+ *   pf_lu_eliminate   rows by records {pos_ik, pos_kk, u0, u1} (int32[4]) and
+ *                     update pairs {pos_kj, pos_ij} (int32[2]): l = m_ik / u_kk,
+ *                     m_ik = l, m_ij -= l u_kj; rec_ptr[n_rows + 1]
+ *   pf_lu_tail_gather dense trailing block t[K][D][D] (tail_pos[D*D], -1 = zero)
+ *   pf_lu_rhs         y(i) = alpha g(P[i])
+ *   pf_lu_forward     rows[]: y_i -= sum m_ik y_k, k < min(i, col_end)
+ *   pf_lu_backward    rows[]: y_i = (y_i - sum_{j > i} m_ij y_j) / m_ii
+ *   pf_lu_tail_vec    entries [t0, t0 + D) of y <-> v[K][D] (to_dense = 1: y -> v)
+ *   pf_lu_apply       state(Q[j]) += x(j) where active[s] (NULL: all)
+ *   pf_lu_residual    max_i |g_i + (J x)_i| per scenario
+ * Device pointers; asynchronous on `stream`. */
+PF_API int pf_lu_scatter(int32_t K, int32_t nnz_a, int32_t nnz_m, const int32_t* a2m,
+                         const double* a, double* m, void* stream);
+PF_API int pf_lu_eliminate(int32_t K, int32_t nnz_m, int32_t n_rows, const int32_t* rec_ptr,
+                           const int32_t* rec, const int32_t* upd, double* m, void* stream);
+PF_API int pf_lu_tail_gather(int32_t K, int32_t nnz_m, int32_t D, const int32_t* tail_pos,
+                             const double* m, double* t, void* stream);
+PF_API int pf_lu_rhs(int32_t K, int32_t n, const int32_t* P, const double* g, double* y,
+                     double alpha, void* stream);
+PF_API int pf_lu_forward(int32_t K, int32_t n, int32_t nnz_m, int32_t n_rows, const int32_t* rows,
+                         const int32_t* m_ptr, const int32_t* m_idx, int32_t col_end,
+                         const double* m, double* y, void* stream);
+PF_API int pf_lu_backward(int32_t K, int32_t n, int32_t nnz_m, int32_t n_rows,
+                          const int32_t* rows, const int32_t* m_ptr, const int32_t* m_diag,
+                          const int32_t* m_idx, const double* m, double* y, void* stream);
+PF_API int pf_lu_tail_vec(int32_t K, int32_t n, int32_t t0, int32_t D, double* y, double* v,
+                          int32_t to_dense, void* stream);
+PF_API int pf_lu_apply(int32_t K, int32_t n, const int32_t* Q, const double* x, double* state,
+                       const int32_t* active, void* stream);
+/* res[s] = max_i |g_i + sum_j J_ij x_j| for scenario s (J: CSR values of the
+ * plan pattern, all blocked): the accuracy check of a batched solve. */
+PF_API int pf_lu_residual(int32_t K, int32_t n, int32_t nnz, const int32_t* csr_ptr,
+                          const int32_t* csr_idx, const double* jv, const double* x,
+                          const double* g, double* res, void* stream);
+
 /* Number of kernels this library has launched (process-wide counter). */
 PF_API int64_t pf_launch_count(void);
 

@@ -104,6 +104,19 @@ _SIGS = {
     "pf_sincos": (C.c_int, [C.c_int64, _VP, _VP, _VP, _VP]),
     "pf_batch_unblock": (C.c_int, [C.c_int32, C.c_int32, _VP, _VP, C.c_double, _VP]),
     "pf_batch_update": (C.c_int, [C.c_int32, C.c_int32, _VP, _VP, _VP, _VP]),
+    "pf_lu_scatter": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP]),
+    "pf_lu_eliminate": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP, _VP]),
+    "pf_lu_tail_gather": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP]),
+    "pf_lu_rhs": (C.c_int, [C.c_int32, C.c_int32, _VP, _VP, _VP, C.c_double, _VP]),
+    "pf_lu_forward": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP,
+                                C.c_int32, _VP, _VP, _VP]),
+    "pf_lu_backward": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP,
+                                 _VP, _VP, _VP, _VP]),
+    "pf_lu_tail_vec": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _VP, _VP, C.c_int32,
+                                 _VP]),
+    "pf_lu_apply": (C.c_int, [C.c_int32, C.c_int32, _VP, _VP, _VP, _VP, _VP]),
+    "pf_lu_residual": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP, _VP, _VP,
+                                 _VP]),
     "pf_launch_count": (C.c_int64, []),
 }
 

@@ -47,9 +47,10 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from . import _abi
-from .plan import Plan
+from .plan import PF_LANES, Plan
 
 _DIVERGENCE_LIMIT = 1e6   # pflow/newton.py:23
+_LIN_RTOL = 1e-10         # accepted residual of a device solve, relative to max|g|
 
 # cusolverRf enums (cusolverRf.h)
 _RF_FORMAT_CSR = 0
@@ -114,12 +115,54 @@ def _ck(status: int, what: str) -> None:
         raise RuntimeError(f"{what} failed (cusolverStatus {status})")
 
 
-def base_lu(csc: sp.csc_matrix, seed: int = 0):
+def robust_row_match(csr: sp.csr_matrix, n_bus: int):
+    """Row order that puts outage-proof entries on the diagonal.
+
+    Every generator row (g_V, g_theta: rows >= 2N, a single entry of value 1)
+    goes to its only column (V_i or theta_i). Every generator column (Q_g,
+    P_s: columns >= 2N, a single entry of value 1 in row g_q[i] or g_p[i])
+    takes that row. The remaining bus rows keep their own diagonal, which is
+    a sum over the bus's branches. No single outage can zero such a pivot, so
+    one pivot order serves every contingency scenario. Returns the row order,
+    or None when the structure does not allow it (for example two generators
+    regulating one bus, which makes the Jacobian singular anyway)."""
+    n = csr.shape[0]
+    row_of = np.full(n, -1, np.int64)       # column -> matched row
+    used = np.zeros(n, bool)
+    csc = csr.tocsc()
+    for r in range(2 * n_bus, n):
+        cols = csr.indices[csr.indptr[r]:csr.indptr[r + 1]]
+        if cols.size != 1 or row_of[cols[0]] >= 0:
+            return None
+        row_of[cols[0]] = r
+        used[r] = True
+    for c in range(2 * n_bus, n):
+        rows = csc.indices[csc.indptr[c]:csc.indptr[c + 1]]
+        rows = rows[rows < 2 * n_bus]
+        if rows.size != 1 or used[rows[0]] or row_of[c] >= 0:
+            return None
+        row_of[c] = rows[0]
+        used[rows[0]] = True
+    for i in range(2 * n_bus):
+        if row_of[i] < 0:
+            if used[i]:
+                return None
+            row_of[i] = i
+            used[i] = True
+    if not used.all():
+        return None
+    return row_of
+
+
+def base_lu(csc: sp.csc_matrix, seed: int = 0, n_bus: int | None = None):
     """Fixed pivoting and a closed symbolic pattern for cusolverRf.
 
     1. SuperLU on the actual base matrix, minimum degree on A^T + A with
        diagonal-preferring pivoting, gives the row / column orders: P, Q with
-       M = A[P][:, Q] factorisable without further pivoting.
+       M = A[P][:, Q] factorisable without further pivoting. With ``n_bus``
+       the rows are first matched to outage-proof diagonals
+       (``robust_row_match``) and SuperLU keeps the diagonal (symmetric mode,
+       no threshold pivoting).
     2. The factor pattern must contain every entry that the numeric
        refactorisation can fill. SuperLU stores no exact zeros, so cancellation
        in step 1 would lose positions. The pattern is therefore recomputed on M
@@ -128,9 +171,17 @@ def base_lu(csc: sp.csc_matrix, seed: int = 0):
     Returns CSR L (unit diagonal stored) and U with that pattern (their values
     are placeholders: every use refactors first), and P, Q."""
     A = csc.tocsc()
-    lu = spla.splu(A, permc_spec="MMD_AT_PLUS_A", options=dict(DiagPivotThresh=0.001))
-    P = np.argsort(lu.perm_r).astype(np.int32)
-    Q = np.argsort(lu.perm_c).astype(np.int32)
+    match = robust_row_match(A.tocsr(), n_bus) if n_bus is not None else None
+    if match is not None:
+        A0 = sp.csr_matrix(A)[match].tocsc()
+        lu = spla.splu(A0, permc_spec="MMD_AT_PLUS_A",
+                       options=dict(DiagPivotThresh=0.0, SymmetricMode=True))
+        P = match[np.argsort(lu.perm_r)].astype(np.int32)
+        Q = np.argsort(lu.perm_c).astype(np.int32)
+    else:
+        lu = spla.splu(A, permc_spec="MMD_AT_PLUS_A", options=dict(DiagPivotThresh=0.001))
+        P = np.argsort(lu.perm_r).astype(np.int32)
+        Q = np.argsort(lu.perm_c).astype(np.int32)
     M = sp.csr_matrix(A)[P][:, Q].tocsr()
     rng = np.random.default_rng(seed)
     M.data = rng.uniform(0.5, 1.0, M.nnz)
@@ -246,6 +297,18 @@ class BatchedLU:
             pass
 
 
+def _host_solve(plan, K, j, g, sc, indptr, indices):
+    """Scenario ``sc``'s Newton step on the host with SuperLU (own pivoting);
+    None when its Jacobian is singular."""
+    n, nnz = plan.n_var, plan.nnz
+    jv = j.view(-1, nnz, PF_LANES)[sc // PF_LANES, :, sc % PF_LANES].cpu().numpy()
+    gv = g.view(-1, n, PF_LANES)[sc // PF_LANES, :, sc % PF_LANES].cpu().numpy()
+    try:
+        return spla.splu(sp.csr_matrix((jv, indices, indptr), shape=(n, n)).tocsc()).solve(-gv)
+    except RuntimeError:
+        return None
+
+
 @dataclass
 class BatchedResult:
     converged: np.ndarray          # [K] bool
@@ -258,10 +321,16 @@ class BatchedResult:
 
 def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None, outage=None,
                          tol: float = 1e-8, max_iter: int = 20, lu: BatchedLU | None = None,
-                         ) -> BatchedResult:
+                         linear: str = "device") -> BatchedResult:
     """Newton on K scenarios in place on the blocked state ``y`` (CUDA
     float64, plan layout).  Returns per-scenario outcomes; ``y`` holds each
-    scenario's last iterate."""
+    scenario's last iterate.
+
+    ``linear="device"`` (default): one elimination schedule shared by all
+    scenarios (batched_lu.py), with outage-proof pivots
+    (``robust_row_match``); a singular scenario shows up as a non-finite
+    mismatch and is reported diverged.  ``linear="cusolverrf"``: one
+    cusolverRf handle per scenario, each with its own pivoting."""
     import torch
 
     if tol <= 0 or max_iter < 1:
@@ -274,7 +343,29 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
     norms = plan.empty(K)
     active = torch.ones(K, dtype=torch.int32, device=dev)
     timings = {"eval": 0.0, "handoff": 0.0, "lu": 0.0, "update": 0.0, "setup": 0.0}
-    if lu is None:   # pivoting and factor pattern of each scenario at its initial state
+    if linear not in ("device", "cusolverrf"):
+        raise ValueError("linear must be 'device' or 'cusolverrf'")
+    dlu = None
+    if linear == "device" and lu is None:
+        # one schedule for every scenario: pivoting from scenario 0 at the
+        # initial state without its outage (an outage can island buses)
+        from .batched_lu import DeviceSparseLU, analyze
+
+        t0 = time.perf_counter()
+        indptr, indices = plan.pattern_csr()
+        plan.eval_batched(K, y, pq_p, pq_q, pv_p, None, None, j, None)
+        j0 = torch.empty(nnz, dtype=torch.float64, device=dev)
+        _abi.check(lib.pf_batch_unblock(1, nnz, j.data_ptr(), j0.data_ptr(), 1.0, None))
+        base = sp.csr_matrix((j0.cpu().numpy(), indices, indptr), shape=(n, n))
+        L, U, P, Q = base_lu(base.tocsc(), n_bus=plan.n_bus)
+        dlu = DeviceSparseLU(analyze(indptr, indices, L, U, P, Q), K, device=dev)
+        indptr_h, indices_h = indptr, indices
+        csr_ptr = torch.as_tensor(indptr, dtype=torch.int32, device=dev)
+        csr_idx = torch.as_tensor(indices, dtype=torch.int32, device=dev)
+        res = plan.empty(K)
+        torch.cuda.synchronize(dev)
+        timings["setup"] = time.perf_counter() - t0
+    elif lu is None:   # pivoting and factor pattern of each scenario at its initial state
         t0 = time.perf_counter()
         indptr, indices = plan.pattern_csr()
         plan.eval_batched(K, y, pq_p, pq_q, pv_p, outage, None, j, None)
@@ -287,6 +378,7 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
     conv = np.zeros(K, dtype=bool)
     div = np.zeros(K, dtype=bool)
     singular = np.zeros(K, dtype=bool)
+    host_solves = 0
     iters = np.zeros(K, dtype=np.int64)
     mism = np.full(K, np.inf)
     stream = torch.cuda.current_stream(dev).cuda_stream
@@ -303,6 +395,35 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
         live = ~(conv | div | singular)
         if not live.any() or it == max_iter:
             break
+        if dlu is not None:   # refactor all scenarios together, update the live ones
+            t0 = time.perf_counter()
+            dlu.factor(j)
+            dx = dlu.solve(g)
+            # accuracy check of every solve: the shared pivot order can fail for
+            # a scenario whose outage makes a pivot vanish after elimination;
+            # those few are solved on the host with their own pivoting
+            _abi.check(lib.pf_lu_residual(K, n, nnz, csr_ptr.data_ptr(), csr_idx.data_ptr(),
+                                          j.data_ptr(), dx.data_ptr(), g.data_ptr(),
+                                          res.data_ptr(), stream))
+            rh = res[:K].cpu().numpy()
+            timings["lu"] += time.perf_counter() - t0
+            t0 = time.perf_counter()
+            ok = live & np.isfinite(rh) & (rh <= _LIN_RTOL * np.maximum(nh, 1e-300))
+            active.copy_(torch.as_tensor(ok.astype(np.int32)))
+            dlu.add(dx, y, active)
+            for sc in np.nonzero(live & ~ok)[0]:
+                dy = _host_solve(plan, K, j, g, int(sc), indptr_h, indices_h)
+                if dy is None:              # singular: pflow's solve raises here
+                    singular[sc] = True
+                    live[sc] = False
+                    continue
+                yv = y.view(-1, n, PF_LANES)
+                yv[sc // PF_LANES, :, sc % PF_LANES] += torch.as_tensor(dy, device=dev)
+                host_solves += 1
+            iters[live] += 1
+            torch.cuda.synchronize(dev)
+            timings["update"] += time.perf_counter() - t0
+            continue
         t0 = time.perf_counter()
         _abi.check(lib.pf_batch_unblock(K, nnz, j.data_ptr(), lu.vals.data_ptr(), 1.0, stream))
         _abi.check(lib.pf_batch_unblock(K, n, g.data_ptr(), lu.rhs.data_ptr(), -1.0, stream))
@@ -322,5 +443,6 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
         iters[live] += 1
         timings["update"] += time.perf_counter() - t0
     torch.cuda.synchronize(dev)
+    timings["host_fallback_solves"] = host_solves
     return BatchedResult(converged=conv, diverged=div, iterations=iters, final_mismatch=mism,
                          singular=singular, timings=timings)

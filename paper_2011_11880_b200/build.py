@@ -25,6 +25,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hi
 UNITS = {
     "pf_eval.cu": ["-fmad=false"],
     "pf_plan.cu": [],
+    "pf_lu.cu": [],
 }
 
 

@@ -1,11 +1,14 @@
 """Batched Newton on the device vs pflow's loop on the CPU.
 
-Workload: a config-0-shaped synthetic grid (2,000 buses, 2,500 branches) with
+Usage: ``batched_newton_bench.py [K] [n_bus] [device|cusolverrf]``.
+
+Workload: a config-0-shaped synthetic grid (default 2,000 buses, 2,500 branches) with
 loads scaled to 5 % so that Newton converges from a flat start; K scenarios
 from ``synth.make_scenarios`` (load / PV scaling, one outage each).
 
-* GPU: ``batched_newton_solve``. Evaluation runs through pf_eval_batched;
-  each scenario's refactorisation and solve run through cusolverRf.
+* GPU: ``batched_newton_solve``. Evaluation runs through pf_eval_batched.
+  The linear solves use the batched sparse LU on the device (``device``, the
+  default) or one cusolverRf handle per scenario (``cusolverrf``).
 * CPU: pflow/newton.py's loop restated on the C oracle (wf1 g and J) with
   SuperLU, one scenario after another, on one core.
 
@@ -38,7 +41,9 @@ def main():
     from paper_2011_11880_b200.system_model import build_system, flat_start
 
     K = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-    s = build_system(_light_case(2000, 2500, seed=0))
+    nb = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
+    linear = sys.argv[3] if len(sys.argv) > 3 else "device"
+    s = build_system(_light_case(nb, nb * 5 // 4, seed=0))
     plan = Plan(s)
     o = oracle.Oracle(s)
     sb = synth.make_scenarios(s, K, seed=1)
@@ -48,11 +53,11 @@ def main():
     args = (t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), torch.as_tensor(sb.outage, device="cuda"))
     # warm-up (library load, kernels)
     yw = dev(to_blocked(np.tile(y0, (K, 1))))
-    batched_newton_solve(plan, K, yw, *args)
+    batched_newton_solve(plan, K, yw, *args, linear=linear)
     y = dev(to_blocked(np.tile(y0, (K, 1))))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = batched_newton_solve(plan, K, y, *args)
+    res = batched_newton_solve(plan, K, y, *args, linear=linear)
     torch.cuda.synchronize()
     gpu_s = time.perf_counter() - t0
     Y = from_blocked(y.cpu().numpy(), K, plan.n_var)
@@ -65,10 +70,14 @@ def main():
     same_it = sum(int(st == "converged" and res.converged[k] and res.iterations[k] == it)
                   for k, (st, it, _) in enumerate(cpu))
     conv = [k for k, (st, _, _) in enumerate(cpu) if st == "converged" and res.converged[k]]
-    dmax = max((float(np.abs(Y[k] - cpu[k][2]).max()) for k in conv), default=None)
+    diffs = {k: float(np.abs(Y[k] - cpu[k][2]).max()) for k in conv}
+    dmax = max(diffs.values(), default=None)
+    worst = sorted(diffs.items(), key=lambda kv: -kv[1])[:3]
+    worst = [(k, v, int(np.abs(Y[k] - cpu[k][2]).argmax()), float(Y[k][int(np.abs(Y[k] - cpu[k][2]).argmax())]),
+              float(cpu[k][2][int(np.abs(Y[k] - cpu[k][2]).argmax())]), int(sb.outage[k])) for k, v in worst]
     line = {
-        "workload": f"2,000-bus synthetic grid (loads x0.05), K={K} scenarios, Newton from flat "
-                    "start, tol 1e-8",
+        "workload": f"{nb}-bus synthetic grid (loads x0.05), K={K} scenarios, Newton from flat "
+                    "start, tol 1e-8", "linear": linear,
         "n_var": plan.n_var, "nnz": plan.nnz,
         "gpu_s": gpu_s, "gpu_timings_s": res.timings,
         "gpu_scenarios_per_s": K / gpu_s,
@@ -76,8 +85,8 @@ def main():
         "converged_gpu": int(res.converged.sum()), "singular_gpu": int(res.singular.sum()),
         "converged_cpu": sum(int(st == "converged") for st, _, _ in cpu),
         "outcome_agreement": agree, "same_iterations": same_it,
-        "max_abs_state_diff": dmax,
-        "iterations": int(res.iterations.max()),
+        "max_abs_state_diff": dmax, "worst_state_diffs": worst,
+        "iterations": int(res.iterations.max()), "n_bus": s.n_bus,
     }
     print(json.dumps(line))
 

@@ -606,7 +606,8 @@ def _cpu_newton(o, y, pq_p, pq_q, pv_p, outage, tol=1e-8, max_iter=20):
         it += 1
 
 
-def test_batched_newton_vs_cpu_newton():
+@pytest.mark.parametrize("linear", ["device", "cusolverrf"])
+def test_batched_newton_vs_cpu_newton(linear):
     """Device-resident batched Newton (pf_eval_batched + cusolverRf
     refactorisation on the fixed pattern) against pflow's loop restated on the
     CPU oracle with SuperLU, scenario by scenario: same outcome, same
@@ -625,7 +626,8 @@ def test_batched_newton_vs_cpu_newton():
     y_dev = _dev(to_blocked(Y))
     t = lambda a: _dev(to_blocked(np.ascontiguousarray(a.T)))
     outage = torch.as_tensor(sb.outage, device="cuda")
-    res = batched_newton_solve(plan, K, y_dev, t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), outage)
+    res = batched_newton_solve(plan, K, y_dev, t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), outage,
+                               linear=linear)
     Yg = from_blocked(y_dev.cpu().numpy(), K, plan.n_var)
     n_conv = 0
     for k in range(K):
@@ -717,3 +719,45 @@ def test_newton_driver_takes_pflow_style_solver_and_workspaces():
     assert res.converged and res.iterations == int(d["newton_iterations"])
     assert Solver.calls == res.iterations
     assert np.abs(res.y - d["newton_y"]).max() < 1e-8
+
+
+def test_device_batched_sparse_lu_vs_scipy():
+    """Batched sparse LU on the device (shared schedule, scenarios in lanes,
+    dense tail through cuSOLVER): x_s = -J_s^{-1} g_s for every scenario
+    against SciPy's sparse solve, and the numpy restatement of the schedule."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+
+    from paper_2011_11880_b200 import batched_lu as BL
+    from paper_2011_11880_b200.batched_newton import base_lu
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    s = build_system(_light_case(600, 760, seed=8))
+    plan = _plan(s)
+    K = 40
+    sb = synth.make_scenarios(s, K, seed=9, outages=False)
+    t = lambda a: _dev(to_blocked(np.ascontiguousarray(a.T)))
+    g, j = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K)
+    plan.eval_batched(K, t(sb.y), t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), None, g, j, None)
+    torch.cuda.synchronize()
+    J = from_blocked(j.cpu().numpy(), K, plan.nnz)
+    G = from_blocked(g.cpu().numpy(), K, plan.n_var)
+    indptr, indices = plan.pattern_csr()
+    n = plan.n_var
+    base = sp.csr_matrix((J[0], indices, indptr), shape=(n, n))
+    L, U, P, Q = base_lu(base.tocsc())
+    sched = BL.analyze(indptr, indices, L, U, P, Q)
+    assert 0 < sched.D < n
+    lu = BL.DeviceSparseLU(sched, K)
+    lu.factor(j)
+    state = torch.zeros_like(g)
+    lu.solve_update(g, state)
+    torch.cuda.synchronize()
+    X = from_blocked(state.cpu().numpy(), K, n)
+    for k in range(K):
+        A = sp.csr_matrix((J[k], indices, indptr), shape=(n, n)).tocsc()
+        ref = spla.spsolve(A, -G[k])
+        assert np.abs(X[k] - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), k
+        if k < 2:
+            x_np = BL.reference_factor_solve(sched, J[k], -G[k])
+            assert np.abs(X[k] - x_np).max() <= 1e-10 * max(1.0, np.abs(ref).max())
