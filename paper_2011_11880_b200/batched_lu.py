@@ -63,23 +63,15 @@ class LUSchedule:
 
 
 def choose_tail(m_ptr, m_idx, n, min_density=0.3, max_d=1536):
-    """Largest trailing block whose density stays >= min_density (<= max_d)."""
-    best = 0
-    cnt = 0
-    # nnz of the trailing block of size d, incrementally (rows/cols >= n - d)
-    rows = [m_idx[m_ptr[i]:m_ptr[i + 1]] for i in range(n)]
-    for d in range(1, min(n, max_d) + 1):
-        t = n - d
-        # new row t within the block, plus new column t in rows > t
-        cnt += int(np.count_nonzero(rows[t] >= t))
-        for i in range(t + 1, n):
-            r = rows[i]
-            k = np.searchsorted(r, t)
-            if k < r.size and r[k] == t:
-                cnt += 1
-        if cnt >= min_density * d * d:
-            best = d
-    return best
+    """Largest trailing block (<= max_d) with density >= min_density: the
+    block of size d holds the entries with min(row, col) >= n - d."""
+    rows = np.repeat(np.arange(n), np.diff(m_ptr))
+    lo = np.minimum(rows, m_idx)
+    # nnz(d) = #{entries with lo >= n - d}, d = 1..n
+    cnt = np.bincount(n - 1 - lo, minlength=n).cumsum()
+    d = np.arange(1, n + 1)
+    ok = (cnt >= min_density * d.astype(np.float64) ** 2) & (d <= max_d)
+    return int(d[ok].max()) if ok.any() else 0
 
 
 def analyze(indptr, indices, L: sp.csr_matrix, U: sp.csr_matrix, P, Q, D: int | None = None,
