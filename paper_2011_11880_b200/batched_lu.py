@@ -81,12 +81,10 @@ def analyze(indptr, indices, L: sp.csr_matrix, U: sp.csr_matrix, P, Q, D: int | 
     M.sort_indices()
     m_ptr = M.indptr.astype(np.int64)
     m_idx = M.indices.astype(np.int32)
-    m_diag = np.empty(n, np.int64)
-    for i in range(n):
-        r = m_idx[m_ptr[i]:m_ptr[i + 1]]
-        k = np.searchsorted(r, i)
-        assert k < r.size and r[k] == i, "missing diagonal"
-        m_diag[i] = m_ptr[i] + k
+    m_diag = np.searchsorted(np.repeat(np.arange(n, dtype=np.int64), np.diff(m_ptr)) * n
+                             + m_idx, np.arange(n, dtype=np.int64) * (n + 1))
+    if not np.array_equal(m_idx[np.minimum(m_diag, m_idx.size - 1)], np.arange(n)):
+        raise AssertionError("missing diagonal")
     Pinv = np.empty(n, np.int64)
     Pinv[P] = np.arange(n)
     Qinv = np.empty(n, np.int64)
@@ -94,12 +92,13 @@ def analyze(indptr, indices, L: sp.csr_matrix, U: sp.csr_matrix, P, Q, D: int | 
     # A entry (r, c) -> M entry (Pinv[r], Qinv[c])
     a_rows = np.repeat(np.arange(n), np.diff(indptr))
     mi, mj = Pinv[a_rows], Qinv[indices]
-    a2m = np.empty(indices.shape[0], np.int64)
-    for e in range(indices.shape[0]):
-        r = m_idx[m_ptr[mi[e]]:m_ptr[mi[e] + 1]]
-        k = np.searchsorted(r, mj[e])
-        assert k < r.size and r[k] == mj[e], "A entry outside the factor pattern"
-        a2m[e] = m_ptr[mi[e]] + k
+    m_rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(m_ptr))
+    m_keys = m_rows * n + m_idx                  # sorted: CSR with sorted columns
+    a_keys = mi * n + mj
+    a2m = np.searchsorted(m_keys, a_keys)
+    if not (a2m < m_keys.size).all() or not np.array_equal(m_keys[np.minimum(a2m, m_keys.size - 1)],
+                                                           a_keys):
+        raise AssertionError("A entry outside the factor pattern")
     if D is None:
         D = choose_tail(m_ptr, m_idx, n, min_density)
     t0 = n - D
