@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "pf_internal.cuh"
 #include "pf_trig.h"
@@ -261,6 +262,17 @@ struct SplitIncidences<Src, decltype(void(Src::kSplit))> {
     static constexpr bool value = Src::kSplit;
 };
 
+// Sources that hold a bus's first incidences and devices in shared memory
+// (the staged batched kernel) set kStaged.
+template <class Src, class = void>
+struct StagedPrefix {
+    static constexpr bool value = false;
+};
+template <class Src>
+struct StagedPrefix<Src, decltype(void(Src::kStaged))> {
+    static constexpr bool value = Src::kStaged;
+};
+
 // Operand source of the global-memory path: every read goes to HBM/L2/L1.
 template <int S>
 struct GlobalSrc {
@@ -339,30 +351,38 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
             }
         }
     } else {
-        for (int32_t e = rng.x; e < rng.y; ++e) {
-            const int32_t t = e - rng.x;
-            const int4 m = src.meta(e, t);
-            const double tj = src.th_j(m.x, t);
-            const double wj = src.v_j(m.x, t);
-            const IncVals v = inc_vals<S>(tab, m, src.coef(e, t), th_i, v_i, tj, wj, out_l);
+        auto inc_step = [&](const int4 m, const double4 c, const double tj, const double wj) {
+            const IncVals v = inc_vals<S>(tab, m, c, th_i, v_i, tj, wj, out_l);
             inc_fold<MODE>(v, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
             if (MODE & JAC) inc_offdiag(v, m, jw, rp, rq, nb);
+        };
+        int32_t e0 = rng.x;
+        if constexpr (StagedPrefix<Src>::value) {   // operands in shared memory
+            const int32_t ns = src.n_inc_staged();
+            for (int32_t t = 0; t < ns; ++t)
+                inc_step(src.smeta(t), src.scoef(t), src.sth(t), src.sv(t));
+            e0 += ns;
+        }
+        for (int32_t e = e0; e < rng.y; ++e) {
+            const int32_t t = e - rng.x;
+            const int4 m = src.meta(e, t);
+            inc_step(m, src.coef(e, t), src.th_j(m.x, t), src.v_j(m.x, t));
         }
     }
 
-    // devices in pool-segment order: PQ, PV, Slack, Shunt (residual.py:57, 91-109)
-    for (int32_t t = rng.z; t < rng.w; ++t) {
-        const int4 dv = src.dev(t, t - rng.z);
+    // devices in pool-segment order: PQ, PV, Slack, Shunt (residual.py:57, 91-109);
+    // ga..gd fetch the device's operands (a, b) and constants (c, d) lazily
+    auto dev_step = [&](const int4 dv, auto ga, auto gb, auto gc, auto gd) {
         const int32_t k = dv.y;
         if (dv.x == DEV_PQ) {
-            acc_p += -src.dev_a(dv, t - rng.z);
-            acc_q += -src.dev_b(dv, t - rng.z);
+            acc_p += -ga();
+            acc_q += -gb();
         } else if (dv.x == DEV_PV) {
             const int32_t row = 2 * N + k;   // g_V row of the gen (pv_qg = index, plan-checked)
-            acc_p += src.dev_a(dv, t - rng.z);
-            acc_q += src.dev_b(dv, t - rng.z);
+            acc_p += ga();
+            acc_q += gb();
             if (MODE & (RES | NORM)) {
-                const double gv = 0.0 + (v_i - src.dev_c(dv, t - rng.z));
+                const double gv = 0.0 + (v_i - gc());
                 if (MODE & RES) st_out(A.g + ln + row * S, gv);
                 nrm = max(nrm, abs_bits(gv));
             }
@@ -375,11 +395,11 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
             const int32_t ps = k;
             const int32_t row_v = 2 * N + q;
             const int32_t row_t = 2 * N + d.n_gen + ps;
-            acc_p += src.dev_a(dv, t - rng.z);   // P_s
-            acc_q += src.dev_b(dv, t - rng.z);   // Q_g
+            acc_p += ga();   // P_s
+            acc_q += gb();   // Q_g
             if (MODE & (RES | NORM)) {
-                const double gv = 0.0 + (v_i - src.dev_c(dv, t - rng.z));
-                const double gt = 0.0 + (th_i - src.dev_d(dv, t - rng.z));
+                const double gv = 0.0 + (v_i - gc());
+                const double gt = 0.0 + (th_i - gd());
                 if (MODE & RES) {
                     st_out(A.g + ln + row_v * S, gv);
                     st_out(A.g + ln + row_t * S, gt);
@@ -393,7 +413,7 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 jw.put(__ldg(d.gen_row_pos + d.n_gen + ps), 1.0);    // (g_theta, theta)
             }
         } else {  // DEV_SHUNT (kernels.py:236-241, 258-262)
-            const double gsh = src.dev_c(dv, t - rng.z), bsh = src.dev_d(dv, t - rng.z);
+            const double gsh = gc(), bsh = gd();
             const double v2 = v_i * v_i;
             acc_p += -gsh * v2;
             acc_q += bsh * v2;
@@ -402,6 +422,22 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 d_qv += 2.0 * bsh * v_i;
             }
         }
+    };
+    int32_t t0 = rng.z;
+    if constexpr (StagedPrefix<Src>::value) {
+        const int32_t nv = src.n_dev_staged();
+        for (int32_t u = 0; u < nv; ++u) {
+            const int4 dv = src.sdev(u);
+            dev_step(dv, [&] { return src.sdev_a(dv, u); }, [&] { return src.sdev_b(dv, u); },
+                     [&] { return src.sdev_c(u); }, [&] { return src.sdev_d(u); });
+        }
+        t0 += nv;
+    }
+    for (int32_t t = t0; t < rng.w; ++t) {
+        const int32_t u = t - rng.z;
+        const int4 dv = src.dev(t, u);
+        dev_step(dv, [&] { return src.dev_a(dv, u); }, [&] { return src.dev_b(dv, u); },
+                 [&] { return src.dev_c(dv, u); }, [&] { return src.dev_d(dv, u); });
     }
 
     if (MODE & RES) {
@@ -517,6 +553,216 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
             ++blk;
         }
     }
+    if (cur >= 0) flush(cur);
+}
+
+// ---- warp-specialised batched kernel ----------------------------------------
+//
+// k_eval_staged: the product batched path.  Same items, order and arithmetic
+// as k_eval_batched (one warp = one bus x 32 scenarios), but the operands of
+// each item reach the evaluating warp through shared memory: one producer
+// warp per CTA walks the CTA's items ahead of the C consumer warps and, for
+// each, copies the bus's packet (header, incidence and device records,
+// device constants) and its scenario rows (own state, neighbour states,
+// device operands: 256 B each) into that consumer's ring slot with cp.async
+// (16 B per lane, two rows per warp instruction), then arms the slot's
+// "full" mbarrier with cp.async.mbarrier.arrive.  The consumer waits on it,
+// evaluates from shared memory and releases the slot on its "empty"
+// mbarrier.  The dependent global loads of the old kernel's per-item chain
+// (header -> records -> neighbour rows -> device rows) leave the consumers'
+// critical path: they overlap the previous item's arithmetic.  Incidences
+// and devices past the staged ones (plan caps WS_*) are read from global
+// memory as before.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+constexpr int WS_ROW_BYTES = PF_LANES * 8;
+constexpr int WS_SLOT_BYTES = WS_ROWS * WS_ROW_BYTES + 32 * 16;   // rows + packet
+
+// Operand source reading a staged slot (rows + packet in shared memory):
+// the first ni incidences and nv devices of the bus; the rest (and the
+// parallel-branch re-reads) go through the global-memory accessors.
+struct StagedSrc : GlobalSrc<PF_LANES> {
+    static constexpr bool kStaged = true;
+    const double* rw;   // slot rows + lane: row r entry at rw[r * PF_LANES]
+    const int4* pk;     // slot packet
+    int32_t ni, nv;
+    __device__ __forceinline__ int4 hdr0() const { return pk[0]; }
+    __device__ __forceinline__ int4 hdr1() const { return pk[1]; }
+    __device__ __forceinline__ double th_i() const { return rw[0]; }
+    __device__ __forceinline__ double v_i() const { return rw[PF_LANES]; }
+    __device__ __forceinline__ int32_t n_inc_staged() const { return ni; }
+    __device__ __forceinline__ int32_t n_dev_staged() const { return nv; }
+    __device__ __forceinline__ int4 smeta(int32_t t) const { return pk[3 + t]; }
+    __device__ __forceinline__ double4 scoef(int32_t t) const {
+        const double2* c = reinterpret_cast<const double2*>(pk + 3 + ni + 2 * t);
+        const double2 a = c[0], b = c[1];
+        return make_double4(a.x, a.y, b.x, b.y);
+    }
+    __device__ __forceinline__ double sth(int32_t t) const { return rw[(2 + 2 * t) * PF_LANES]; }
+    __device__ __forceinline__ double sv(int32_t t) const { return rw[(3 + 2 * t) * PF_LANES]; }
+    __device__ __forceinline__ int4 sdev(int32_t u) const { return pk[3 + 3 * ni + u]; }
+    __device__ __forceinline__ double2 scd(int32_t u) const {
+        return reinterpret_cast<const double2*>(pk + 3 + 3 * ni + nv)[u];
+    }
+    // rows a / b: PQ (pq_p, pq_q), PV (pv_p, Q_g), Slack (P_s, Q_g); a scenario
+    // array the caller did not pass falls back to the plan constants
+    // (packet: PQ {p0, q0}, PV {v0, p0}, Slack {v0, theta0}, Shunt {g, b})
+    __device__ __forceinline__ double sdev_a(const int4 dv, int32_t u) const {
+        const double r = rw[(2 + 2 * ni + 2 * u) * PF_LANES];
+        if (dv.x == DEV_PQ) return A.pq_p ? r : scd(u).x;
+        if (dv.x == DEV_PV) return A.pv_p ? r : scd(u).y;
+        return r;
+    }
+    __device__ __forceinline__ double sdev_b(const int4 dv, int32_t u) const {
+        const double r = rw[(3 + 2 * ni + 2 * u) * PF_LANES];
+        if (dv.x == DEV_PQ) return A.pq_q ? r : scd(u).y;
+        return r;
+    }
+    __device__ __forceinline__ double sdev_c(int32_t u) const { return scd(u).x; }
+    __device__ __forceinline__ double sdev_d(int32_t u) const { return scd(u).y; }
+};
+
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Issue the copies of one item into slot sb: lane l holds word (l & 15) of
+// the item's stage record in `rw`.  The packet goes 16 B per lane, the rows
+// 16 lanes per row (two rows per instruction).  One commit group per item.
+__device__ __forceinline__ void stage_item(unsigned char* sb, const int32_t rw,
+                                           const int4* __restrict__ pkt, const double* b0,
+                                           const double* b1, const double* b2, const double* b3,
+                                           const int lane) {
+    const int32_t off = __shfl_sync(0xffffffffu, rw, 0);
+    const int32_t meta = __shfl_sync(0xffffffffu, rw, 1);
+    const int32_t units = meta & 0xffff, rows = meta >> 16;
+    if (lane < units) cp_async16(sb + WS_ROWS * WS_ROW_BYTES + lane * 16, pkt + off + lane);
+    const int half = lane >> 4, chunk = lane & 15;
+    for (int rr0 = 0; rr0 < rows; rr0 += 2) {
+        const int rr = rr0 + half;
+        const int32_t cd = __shfl_sync(0xffffffffu, rw, 2 + rr);
+        const uint32_t arr = (uint32_t)cd >> 29;
+        const double* bp = arr == 0 ? b0 : arr == 1 ? b1 : arr == 2 ? b2 : b3;
+        if (rr < rows && cd >= 0 && bp)
+            cp_async16(sb + rr * WS_ROW_BYTES + chunk * 16,
+                       bp + (int64_t)(cd & 0x1fffffff) * PF_LANES + chunk * 2);
+    }
+    cp_async_commit();
+}
+
+// Each warp stages its own next item (no producer warp, no cross-warp
+// coupling): at the start of item k it issues item k+1's copies into its
+// other slot and loads item k+2's stage record, then waits for item k's
+// copies (issued one item earlier) and evaluates from shared memory.
+template <int MODE, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
+    const DevicePlan d, const int32_t K, const int32_t n_groups, const int32_t n_items,
+    const double* __restrict__ y, const double* __restrict__ pq_p,
+    const double* __restrict__ pq_q, const double* __restrict__ pv_p,
+    const int32_t* __restrict__ outage, double* __restrict__ g, double* __restrict__ jv,
+    unsigned long long* __restrict__ norms, const uint32_t fd_m, const uint32_t fd_l) {
+    extern __shared__ __align__(128) unsigned char ws_smem[];
+    __shared__ double s_tab[PF_TRIG_N * 4];
+    __shared__ Scen<PF_LANES> As[W];   // per-warp block base pointers
+    const double* tab = stage_trig_table(s_tab);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Scen<PF_LANES>& A = As[warp];
+    unsigned char* slots = ws_smem + (size_t)warp * 2 * WS_SLOT_BYTES;
+
+    // items are walked with a stride of gridDim.x; item -> (block, group)
+    // by multiply-shift division (fd_m, fd_l: n_groups), so the look-ahead
+    // costs no loop-carried registers.  The warp's bus slot is grp * W + warp.
+    const int32_t stride = gridDim.x;
+    auto blk_of = [&](int32_t it) -> int32_t {
+        return (int32_t)((__umulhi((uint32_t)it, fd_m) + (uint32_t)it) >> fd_l);
+    };
+    auto rec_word = [&](int32_t it) -> int32_t {
+        if (it >= n_items) return -1;
+        const int32_t slot = (it - blk_of(it) * n_groups) * W + warp;
+        if (slot >= d.N) return -1;
+        return __ldg(reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
+                     (lane & 15));
+    };
+    auto issue = [&](int32_t it, int32_t rw, unsigned char* sb) {
+        if (it < n_items && __shfl_sync(0xffffffffu, rw, 0) >= 0) {
+            const int64_t bb = blk_of(it);
+            stage_item(sb, rw, d.ws_pkt, y + bb * d.n_var * PF_LANES,
+                       pq_p ? pq_p + bb * d.P * PF_LANES : nullptr,
+                       pq_q ? pq_q + bb * d.P * PF_LANES : nullptr,
+                       pv_p ? pv_p + bb * d.G * PF_LANES : nullptr, lane);
+        } else {
+            cp_async_commit();   // keep one group per item
+        }
+    };
+
+    // norms: each warp keeps a per-lane running max over its items of the
+    // current scenario block and max-es it into norms[] when it leaves the
+    // block (integer max of |g| bit patterns: exact, order-independent).  No
+    // CTA barrier: warps cross block boundaries independently.
+    int32_t cur = -1;
+    unsigned long long nrm = 0;
+    auto flush = [&](int32_t blk) {
+        if (MODE & NORM) {
+            const int32_t s = blk * PF_LANES + lane;
+            if (s < K && nrm) atomicMax(norms + s, nrm);
+        }
+        nrm = 0;
+    };
+    int32_t out_l = -1;
+    // prologue: item 0's copies in flight, item 1's record in a register
+    issue(blockIdx.x, rec_word(blockIdx.x), slots);
+    int32_t rw_next = rec_word(blockIdx.x + stride);
+    int32_t k = 0;
+    for (int32_t item = blockIdx.x; item < n_items; item += stride, ++k) {
+        const int32_t blk = blk_of(item);
+        const int32_t grp = item - blk * n_groups;
+        if (blk != cur) {
+            if (cur >= 0) flush(cur);
+            cur = blk;
+            if (lane == 0) {
+                const int64_t b = blk;
+                A.y = y + b * d.n_var * PF_LANES;
+                A.g = g ? g + b * d.n_var * PF_LANES : nullptr;
+                A.j = jv ? jv + b * d.nnz * PF_LANES : nullptr;
+                A.pq_p = pq_p ? pq_p + b * d.P * PF_LANES : nullptr;
+                A.pq_q = pq_q ? pq_q + b * d.P * PF_LANES : nullptr;
+                A.pv_p = pv_p ? pv_p + b * d.G * PF_LANES : nullptr;
+            }
+            const int32_t s = blk * PF_LANES + lane;
+            out_l = (outage && s < K) ? __ldg(outage + s) : -1;
+            __syncwarp();
+        }
+        unsigned char* sb = slots + (k & 1) * WS_SLOT_BYTES;
+        // next item's copies into the other slot (its previous contents,
+        // item k-1, were consumed in the previous iteration), then the
+        // record of the item after it
+        issue(item + stride, rw_next, slots + ((k + 1) & 1) * WS_SLOT_BYTES);
+        rw_next = rec_word(item + 2 * stride);
+        cp_async_wait<1>();   // this item's group has landed (own lanes)
+        __syncwarp();         // ... and every lane's
+        const int32_t slot = grp * W + warp;
+        if (slot < d.N && blk * PF_LANES + lane < K) {
+            const int4* pk = reinterpret_cast<const int4*>(sb + WS_ROWS * WS_ROW_BYTES);
+            const int4 cnt = pk[2];
+            const StagedSrc src{{d, A, A.y + lane, cnt.z, lane},
+                                reinterpret_cast<const double*>(sb) + lane, pk, cnt.x, cnt.y};
+            nrm = max(nrm, eval_bus_src<MODE, PF_LANES>(
+                               d, tab, cnt.z, src, A, lane, out_l,
+                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}));
+        }
+        __syncwarp();         // slot reads done before it is refilled
+    }
+    cp_async_wait<0>();
     if (cur >= 0) flush(cur);
 }
 
@@ -1130,6 +1376,54 @@ static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const dou
     return cudaSuccess;
 }
 
+// Staged kernel shape: 12 warps per CTA, 2 CTAs per SM (24 warps at <= 80
+// registers), two 4 KB slots per warp (96 KB of shared memory per CTA).
+constexpr int WS_W = 12;
+constexpr int WS_MINB = 2;
+constexpr size_t WS_SMEM = (size_t)WS_W * 2 * WS_SLOT_BYTES;
+template <int MODE>
+static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const double* y,
+                                      const double* pq_p, const double* pq_q,
+                                      const double* pv_p, const int32_t* outage, double* g,
+                                      double* j, double* norms, cudaStream_t st) {
+    auto kern = k_eval_staged<MODE, WS_W, WS_MINB>;
+    static int ctas = 0;
+    static int sms = 0;
+    if (!ctas) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, 32 * WS_W, WS_SMEM);
+        if (ctas < 1) ctas = 1;
+    }
+    const int32_t n_groups = (d.N + WS_W - 1) / WS_W;
+    const int64_t n_items64 = (int64_t)n_groups * ((K + PF_LANES - 1) / PF_LANES);
+    if (n_items64 >= (1ll << 31)) return cudaErrorInvalidValue;
+    const int32_t n_items = (int32_t)n_items64;
+    const int grid = (int)std::min<int64_t>(std::min<int64_t>(n_items, n_groups),
+                                            (int64_t)ctas * sms);
+    // n_groups as a multiply-shift divisor (Granlund-Montgomery, round-up form)
+    uint32_t fd_l = 0;
+    while ((1ll << fd_l) < n_groups) ++fd_l;
+    const uint32_t fd_m =
+        (uint32_t)(((1ull << 32) * ((1ull << fd_l) - (uint64_t)n_groups)) / (uint64_t)n_groups + 1);
+    kern<<<grid, 32 * WS_W, WS_SMEM, st>>>(d, K, n_groups, n_items, y, pq_p, pq_q, pv_p,
+                                           outage, g, j,
+                                           reinterpret_cast<unsigned long long*>(norms), fd_m,
+                                           fd_l);
+    return cudaSuccess;
+}
+
+static bool use_staged() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PF_BATCHED_KERNEL");
+        v = !(e && e[0] == 'o');   // "old": the single-role kernel (A/B timing)
+    }
+    return v == 1;
+}
+
 cudaError_t launch_eval_batched(const DevicePlan& d, int32_t K, const double* y,
                                 const double* pq_p, const double* pq_q, const double* pv_p,
                                 const int32_t* outage, double* g, double* j, double* norms,
@@ -1140,7 +1434,9 @@ cudaError_t launch_eval_batched(const DevicePlan& d, int32_t K, const double* y,
     }
     if (d.N == 0 || K == 0) return cudaSuccess;
     const int mode = (g ? RES : 0) | (j ? JAC : 0) | (norms ? NORM : 0);
-#define PF_B(M) launch_batched_mode<M>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st)
+#define PF_B(M)                                                                         \
+    (use_staged() ? launch_staged_mode<M>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st) \
+                  : launch_batched_mode<M>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st))
     cudaError_t e = cudaSuccess;
     switch (mode) {
         case RES: e = PF_B(RES); break;

@@ -41,6 +41,25 @@ constexpr int32_t SG_FIELD_MASK = 0x3ff;
 constexpr int SG_DUP_SHIFT = 10;
 static_assert(SG_CAP_BUS <= SG_FIELD_MASK + 1 && SG_CAP_DUP <= SG_FIELD_MASK + 1, "sg_inc");
 
+// Batched kernel, warp-specialised (k_eval_staged): a producer warp copies
+// each bus's operands into a consumer warp's shared-memory slot with cp.async.
+// Per bus (processing order) the plan holds a packet of 16-byte units
+//   [0] bus_row[2i]  [1] bus_row[2i+1]  [2] {ni, nv, bus, 0}
+//   [3, 3+ni) inc_meta   [3+ni, 3+3ni) inc_coef   [3+3ni, +nv) dev_list
+//   [3+3ni+nv, +nv) device constants {c, d} (double2)
+// and a stage record of WS_REC_WORDS int32: {packet offset (units),
+// packet units | rows << 16, row code x WS_ROWS} naming the 256-byte scenario
+// rows to stage: 0 theta_i, 1 V_i, 2+2t / 3+2t theta_j / V_j of staged
+// incidence t < ni, 2+2ni+2u / 3+2ni+2u operands a / b of staged device u < nv.
+// Row code = (array << 29) | entry (array 0 y, 1 pq_p, 2 pq_q, 3 pv_p), -1 none.
+// Incidences and devices past the staged ones are read from global memory.
+constexpr int WS_ROWS = 14;
+constexpr int WS_MAXINC = 6;
+constexpr int WS_MAXDEV = 2;
+constexpr int WS_PKT_UNITS = 3 + 3 * WS_MAXINC + 2 * WS_MAXDEV;   // 25
+constexpr int WS_REC_WORDS = 2 + WS_ROWS;                        // 16 (64 bytes)
+static_assert(WS_PKT_UNITS <= 32, "one cp.async per lane covers the packet");
+
 // Device-list entry types, in the reference's pool-segment order (residual.py:57).
 enum DevType : int32_t { DEV_PQ = 0, DEV_PV = 1, DEV_SLACK = 2, DEV_SHUNT = 3 };
 
@@ -67,6 +86,8 @@ struct DevicePlan {
                               // diagonal rank; [2i+1] = {e0, e1, t0, t1}: incidence
                               // and device-list ranges (one 32-byte load)
     const int32_t* bus_order; // [N] batched processing order: degree >= HUB_DEG first
+    const int4* ws_pkt;       // staged-kernel packets (see WS_ROWS above)
+    const int4* ws_rec;       // [N * WS_REC_WORDS / 4] stage records in processing order
     const int32_t* dev_ptr;   // [N+1]
     const int4* dev_list;     // [n_dev] {type, index, jpos_a, jpos_b}
     // device parameters (base values; scenarios may override P/Q)

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <cub/cub.cuh>
 #include <string>
 #include <vector>
@@ -602,8 +603,8 @@ int build(const pf_topology* t, pf_plan** out) {
     P->max_deg = md;
     // batched processing order: high-degree buses first, then the rest, each
     // in bus order (the identity when there are no hubs)
+    std::vector<int32_t> order;
     {
-        std::vector<int32_t> order;
         order.reserve(N);
         for (int32_t i = 0; i < N; ++i)
             if (hptr[i + 1] - hptr[i] >= HUB_DEG) order.push_back(i);
@@ -688,6 +689,108 @@ int build(const pf_topology* t, pf_plan** out) {
         d.sg_inc = dinc;
         d.sg_acc = acc;
         d.sg_count = cnt;
+    }
+    // warp-specialised batched kernel: per bus (processing order) a packet of
+    // its header / staged incidence and device records and a stage record
+    // naming the scenario rows to copy (pf_internal.cuh, WS_ROWS)
+    {
+        std::vector<int4> hmeta(n_inc), hrow(2 * (size_t)N), hdev;
+        std::vector<double4> hcoef(n_inc);
+        const int32_t n_dev = d.P + d.G + d.S + d.H;
+        hdev.resize(n_dev);
+        if (n_inc) {
+            PF_TRY(cudaMemcpy(hmeta.data(), d.inc_meta, sizeof(int4) * (size_t)n_inc,
+                              cudaMemcpyDeviceToHost));
+            PF_TRY(cudaMemcpy(hcoef.data(), d.inc_coef, sizeof(double4) * (size_t)n_inc,
+                              cudaMemcpyDeviceToHost));
+        }
+        if (n_dev)
+            PF_TRY(cudaMemcpy(hdev.data(), d.dev_list, sizeof(int4) * (size_t)n_dev,
+                              cudaMemcpyDeviceToHost));
+        PF_TRY(cudaMemcpy(hrow.data(), d.bus_row, sizeof(int4) * 2 * (size_t)N,
+                          cudaMemcpyDeviceToHost));
+        std::vector<int4> pkt;
+        std::vector<int32_t> rec((size_t)N * WS_REC_WORDS, -1);
+        pkt.reserve((size_t)N * 12);
+        auto code = [](int32_t arr, int64_t e) { return (int32_t)((arr << 29) | (int32_t)e); };
+        auto d2 = [](double a, double b) {
+            int4 u;
+            long long x, y;
+            std::memcpy(&x, &a, 8);
+            std::memcpy(&y, &b, 8);
+            u.x = (int32_t)(x & 0xffffffff); u.y = (int32_t)(x >> 32);
+            u.z = (int32_t)(y & 0xffffffff); u.w = (int32_t)(y >> 32);
+            return u;
+        };
+        for (int32_t s = 0; s < N; ++s) {
+            const int32_t i = order[s];
+            const int4 h0 = hrow[2 * (size_t)i], h1 = hrow[2 * (size_t)i + 1];
+            const int32_t deg = h1.y - h1.x, ndev = h1.w - h1.z;
+            const int32_t nv = std::min(ndev, WS_MAXDEV);
+            const int32_t ni = std::min({deg, WS_MAXINC, (WS_ROWS - 2 - 2 * nv) / 2});
+            int32_t* r = &rec[(size_t)s * WS_REC_WORDS];
+            const int64_t off = (int64_t)pkt.size();
+            if (off >= (1ll << 31)) {
+                free_plan(P);
+                return invalid("staged packets exceed 2^31 units");
+            }
+            pkt.push_back(h0);
+            pkt.push_back(h1);
+            pkt.push_back(make_int4(ni, nv, i, 0));
+            for (int32_t q = 0; q < ni; ++q) pkt.push_back(hmeta[h1.x + q]);
+            for (int32_t q = 0; q < ni; ++q) {
+                const double4 c = hcoef[h1.x + q];
+                pkt.push_back(d2(c.x, c.y));
+                pkt.push_back(d2(c.z, c.w));
+            }
+            int32_t* rows = r + 2;
+            rows[0] = code(0, i);
+            rows[1] = code(0, (int64_t)N + i);
+            for (int32_t q = 0; q < ni; ++q) {
+                const int32_t j = hmeta[h1.x + q].x;
+                rows[2 + 2 * q] = code(0, j);
+                rows[3 + 2 * q] = code(0, (int64_t)N + j);
+            }
+            for (int32_t u = 0; u < nv; ++u) pkt.push_back(hdev[h1.z + u]);
+            for (int32_t u = 0; u < nv; ++u) {
+                const int4 dv = hdev[h1.z + u];
+                const int32_t k = dv.y;
+                int32_t* ra = rows + 2 + 2 * ni + 2 * u;
+                double c = 0.0, dd = 0.0;
+                if (dv.x == DEV_PQ) {          // a = pq_p, b = pq_q; base p0, q0
+                    ra[0] = code(1, k);
+                    ra[1] = code(2, k);
+                    c = t->pq_p0[k];
+                    dd = t->pq_q0[k];
+                } else if (dv.x == DEV_PV) {   // a = pv_p, b = Q_g; v0, base p0
+                    ra[0] = code(3, k);
+                    ra[1] = code(0, 2 * (int64_t)N + k);
+                    c = t->pv_v0[k];
+                    dd = t->pv_p0[k];
+                } else if (dv.x == DEV_SLACK) {  // a = P_s, b = Q_g; v0, theta0
+                    ra[0] = code(0, 2 * (int64_t)N + d.n_gen + k);
+                    ra[1] = code(0, 2 * (int64_t)N + d.G + k);
+                    c = t->sl_v0[k];
+                    dd = t->sl_th0[k];
+                } else {                       // shunt: g, b
+                    c = t->sh_g[k];
+                    dd = t->sh_b[k];
+                }
+                pkt.push_back(d2(c, dd));
+            }
+            r[0] = (int32_t)off;
+            r[1] = (int32_t)(pkt.size() - off) | ((2 + 2 * ni + 2 * nv) << 16);
+        }
+        int4 *dpkt, *drec;
+        PF_TRY(owned_alloc(P, &dpkt, std::max<int64_t>((int64_t)pkt.size(), 1)));
+        PF_TRY(owned_alloc(P, &drec, std::max<int64_t>((int64_t)N * WS_REC_WORDS / 4, 1)));
+        if (!pkt.empty())
+            PF_TRY(cudaMemcpy(dpkt, pkt.data(), sizeof(int4) * pkt.size(), cudaMemcpyHostToDevice));
+        if (N)
+            PF_TRY(cudaMemcpy(drec, rec.data(), sizeof(int32_t) * rec.size(),
+                              cudaMemcpyHostToDevice));
+        d.ws_pkt = dpkt;
+        d.ws_rec = drec;
     }
     count_launch(12);
     *out = P;
