@@ -145,17 +145,19 @@ struct IncVals {
     double opt, opv, oqt, oqv;     // off-diagonal partials (theta_j, V_j)
 };
 
-// The ten values of one terminal from sin/cos of thk = theta_h - theta_k
-// (kernels.py:86-88), the terminal's coefficients c and u = V_i, w = V_j.
-// h side: c = {gl, bl, gsh, bsh}.  k side: c = {gl2, -bl2, gsk, bsk}, so
-// t1 = gl2 ci - bl2 si = t1k and t2 = gl2 si + bl2 ci = t2k, with t2s = -t2k.
-// Sign flips are exact, so every term is bit-identical to kernels.py:90-163.
-__device__ __forceinline__ IncVals inc_terms(const bool kside, const double si, const double ci,
-                                             const double4 c, const double u, const double w) {
+// The ten values of one terminal, from sin/cos of d = theta_i - theta_j
+// (bus i, neighbour j), the terminal's coefficients c and u = V_i, w = V_j.
+// h side (i = h): c = {gl, bl, gsh, bsh} and d = thk (kernels.py:86), so
+// t1 = gl ci + bl si = t1h, t2 = gl si - bl ci = t2h.  k side (i = k):
+// c = {gl2, bl2, gsk, bsk} and d = -thk, so sin d = -sin thk (pf_trig is odd
+// bit for bit) and t1 = gl2 ci - bl2 sin thk = t1k, t2 = -(gl2 sin thk +
+// bl2 ci) = -t2k.  Negations are exact and rounding is sign-symmetric, so
+// every term is bit-identical to kernels.py:90-163 (t2s is t2h | -t2k).
+__device__ __forceinline__ IncVals inc_terms(const double sd, const double ci, const double4 c,
+                                             const double u, const double w) {
     const double ab = u * w;
-    const double t1 = c.x * ci + c.y * si;
-    const double t2 = c.x * si - c.y * ci;
-    const double t2s = kside ? -t2 : t2;
+    const double t1 = c.x * ci + c.y * sd;
+    const double t2s = c.x * sd - c.y * ci;
     const double uu = u * u;                     // (-u)*u == -(u*u) exactly
     IncVals v;
     v.fp = uu * c.z - ab * t1;                   // ph | pk
@@ -182,12 +184,9 @@ __device__ __forceinline__ IncVals inc_vals(const double* tab, const int4 m, dou
         const bool hit = m.y == out_l;
         if (__any_sync(__activemask(), hit) && hit) c = make_double4(0.0, 0.0, 0.0, 0.0);
     }
-    const bool kside = (m.z & KSIDE) != 0;
-    // thk = theta_h - theta_k (kernels.py:86)
-    const double thk = kside ? (th_j - th_i) : (th_i - th_j);
-    double si, ci;
-    pf_sincos(thk, tab, &si, &ci);
-    return inc_terms(kside, si, ci, c, u, w);
+    double sd, ci;
+    pf_sincos(th_i - th_j, tab, &sd, &ci);
+    return inc_terms(sd, ci, c, u, w);
 }
 
 // Fold one incidence into the bus's sums, in list order.
@@ -245,10 +244,19 @@ __device__ __forceinline__ void inc_offdiag(const IncVals& v, const int4 m, cons
                                             const int32_t rp, const int32_t rq, const int32_t nb) {
     const bool first = (m.z & FIRST) != 0;
     const int32_t pos = m.z & POS_MASK;
-    jw.add(rp + pos, first, v.opt);
-    jw.add(rp + nb + pos, first, v.opv);
-    jw.add(rq + pos, first, v.oqt);
-    jw.add(rq + nb + pos, first, v.oqv);
+    // one (warp-uniform) branch per incidence: the common first-neighbour
+    // stores, or the rare parallel-branch read-modify-writes
+    if (first) {
+        jw.add(rp + pos, true, v.opt);
+        jw.add(rp + nb + pos, true, v.opv);
+        jw.add(rq + pos, true, v.oqt);
+        jw.add(rq + nb + pos, true, v.oqv);
+    } else {
+        jw.add(rp + pos, false, v.opt);
+        jw.add(rp + nb + pos, false, v.opv);
+        jw.add(rq + pos, false, v.oqt);
+        jw.add(rq + nb + pos, false, v.oqv);
+    }
 }
 
 // Sources whose incidence values were computed beforehand (the single-grid
@@ -577,9 +585,8 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 constexpr int WS_ROW_BYTES = PF_LANES * 8;
 constexpr int WS_SLOT_BYTES = WS_ROWS * WS_ROW_BYTES + 32 * 16;   // rows + packet
@@ -636,26 +643,32 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Issue the copies of one item into slot sb: lane l holds word (l & 15) of
-// the item's stage record in `rw`.  The packet goes 16 B per lane, the rows
-// 16 lanes per row (two rows per instruction).  One commit group per item.
-__device__ __forceinline__ void stage_item(unsigned char* sb, const int32_t rw,
+// Issue the copies of one item into the slot at shared address sb.  Lane l
+// holds word (l + 2) & 15 of the item's stage record in `rw`: lanes 0..13 the
+// codes of rows 0..13, lanes 14 and 15 the packet offset and sizes.  Each
+// lane decodes its own row's source address once; the packet goes 16 B per
+// lane, the rows 16 lanes per row (two rows per instruction).  One commit
+// group per item.
+__device__ __forceinline__ void stage_item(const uint32_t sb, const int32_t rw,
                                            const int4* __restrict__ pkt, const double* b0,
                                            const double* b1, const double* b2, const double* b3,
                                            const int lane) {
-    const int32_t off = __shfl_sync(0xffffffffu, rw, 0);
-    const int32_t meta = __shfl_sync(0xffffffffu, rw, 1);
+    const int32_t off = __shfl_sync(0xffffffffu, rw, 14);
+    const int32_t meta = __shfl_sync(0xffffffffu, rw, 15);
     const int32_t units = meta & 0xffff, rows = meta >> 16;
     if (lane < units) cp_async16(sb + WS_ROWS * WS_ROW_BYTES + lane * 16, pkt + off + lane);
+    const double* src = nullptr;
+    if (lane < rows && rw >= 0) {
+        const uint32_t arr = (uint32_t)rw >> 29;
+        const double* bp = arr == 0 ? b0 : arr == 1 ? b1 : arr == 2 ? b2 : b3;
+        if (bp) src = bp + (int64_t)(rw & 0x1fffffff) * PF_LANES;
+    }
     const int half = lane >> 4, chunk = lane & 15;
     for (int rr0 = 0; rr0 < rows; rr0 += 2) {
         const int rr = rr0 + half;
-        const int32_t cd = __shfl_sync(0xffffffffu, rw, 2 + rr);
-        const uint32_t arr = (uint32_t)cd >> 29;
-        const double* bp = arr == 0 ? b0 : arr == 1 ? b1 : arr == 2 ? b2 : b3;
-        if (rr < rows && cd >= 0 && bp)
-            cp_async16(sb + rr * WS_ROW_BYTES + chunk * 16,
-                       bp + (int64_t)(cd & 0x1fffffff) * PF_LANES + chunk * 2);
+        const double* p = reinterpret_cast<const double*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), rr));
+        if (rr < rows && p) cp_async16(sb + rr * WS_ROW_BYTES + chunk * 16, p + chunk * 2);
     }
     cp_async_commit();
 }
@@ -678,6 +691,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Scen<PF_LANES>& A = As[warp];
     unsigned char* slots = ws_smem + (size_t)warp * 2 * WS_SLOT_BYTES;
+    const uint32_t slots_u32 = smem_u32(slots);
 
     // items are walked with a stride of gridDim.x; item -> (block, group)
     // by multiply-shift division (fd_m, fd_l: n_groups), so the look-ahead
@@ -691,10 +705,10 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         const int32_t slot = (it - blk_of(it) * n_groups) * W + warp;
         if (slot >= d.N) return -1;
         return __ldg(reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
-                     (lane & 15));
+                     ((lane + 2) & 15));
     };
-    auto issue = [&](int32_t it, int32_t rw, unsigned char* sb) {
-        if (it < n_items && __shfl_sync(0xffffffffu, rw, 0) >= 0) {
+    auto issue = [&](int32_t it, int32_t rw, uint32_t sb) {
+        if (it < n_items && __shfl_sync(0xffffffffu, rw, 14) >= 0) {
             const int64_t bb = blk_of(it);
             stage_item(sb, rw, d.ws_pkt, y + bb * d.n_var * PF_LANES,
                        pq_p ? pq_p + bb * d.P * PF_LANES : nullptr,
@@ -720,7 +734,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     };
     int32_t out_l = -1;
     // prologue: item 0's copies in flight, item 1's record in a register
-    issue(blockIdx.x, rec_word(blockIdx.x), slots);
+    issue(blockIdx.x, rec_word(blockIdx.x), slots_u32);
     int32_t rw_next = rec_word(blockIdx.x + stride);
     int32_t k = 0;
     for (int32_t item = blockIdx.x; item < n_items; item += stride, ++k) {
@@ -746,7 +760,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         // next item's copies into the other slot (its previous contents,
         // item k-1, were consumed in the previous iteration), then the
         // record of the item after it
-        issue(item + stride, rw_next, slots + ((k + 1) & 1) * WS_SLOT_BYTES);
+        issue(item + stride, rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
         rw_next = rec_word(item + 2 * stride);
         cp_async_wait<1>();   // this item's group has landed (own lanes)
         __syncwarp();         // ... and every lane's

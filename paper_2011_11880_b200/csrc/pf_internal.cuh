@@ -80,7 +80,7 @@ struct DevicePlan {
     const int32_t* inc_ptr;   // [N+1]
     const int4* inc_meta;     // [n_inc] {neighbour j, branch l, pos|flags, owning bus}
     const double4* inc_coef;  // [n_inc] {g1, b1, gs, bs}: h side {gl, bl, gsh, bsh},
-                              //          k side {gl2, -bl2, gsk, bsk}
+                              //          k side {gl2, bl2, gsk, bsk}
     const int4* bus_row;      // [2N] bus header: [2i] = {rp, rq, nb, pos_i|VDIAG}: CSR
                               // offsets of rows g_p[i], g_q[i], theta-block size,
                               // diagonal rank; [2i+1] = {e0, e1, t0, t1}: incidence

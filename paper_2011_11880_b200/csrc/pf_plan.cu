@@ -96,7 +96,7 @@ __global__ void k_inc_records(int32_t L, const int32_t* sorted_e, const int32_t*
     bool ks = e >= L;
     int32_t l = ks ? e - L : e;
     meta[t] = make_int4(ks ? bh[l] : bk[l], l, ks ? KSIDE : 0, ks ? bk[l] : bh[l]);
-    coef[t] = ks ? make_double4(gl2[l], -bl2[l], gsk[l], bsk[l])
+    coef[t] = ks ? make_double4(gl2[l], bl2[l], gsk[l], bsk[l])
                  : make_double4(gl[l], bl[l], gsh[l], bsh[l]);
 }
 

@@ -73,13 +73,16 @@ PF_HD void pf_two_sum(double a, double b, double* s, double* e) {
  * in shared memory by the caller). */
 PF_HD void pf_sincos_tab(double x, const double* tab, double* sp, double* cp) {
     if (!(fabs(x) < 1048576.0)) {
+        /* evaluated at |x| so that, like the fast path, sin is odd and cos
+         * even bit for bit (the kernels evaluate one branch terminal at
+         * -thk, pf_eval.cu inc_terms) */
 #ifdef __CUDA_ARCH__
-        const double2 r = pf_sincos_slow(x);
-        *sp = r.x;
+        const double2 r = pf_sincos_slow(fabs(x));
+        *sp = x < 0.0 ? -r.x : r.x;
         *cp = r.y;
 #else
-        *sp = sin(x);
-        *cp = cos(x);
+        *sp = x < 0.0 ? -sin(-x) : sin(x);
+        *cp = cos(fabs(x));
 #endif
         return;
     }

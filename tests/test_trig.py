@@ -70,3 +70,13 @@ def test_special_values(twin):
     s, c = twin_sincos(twin, x)
     assert np.isnan(s[:3]).all() and np.isnan(c[:3]).all()
     assert s[3] == np.sin(2.0 ** 30) or abs(s[3] - np.sin(2.0 ** 30)) < 1e-15
+
+
+def test_twin_odd_even_bit_for_bit(twin):
+    """sin(-x) == -sin(x) and cos(-x) == cos(x) exactly, fast and slow paths:
+    the kernels evaluate a branch's k terminal at -thk (pf_eval.cu inc_terms)."""
+    x = np.concatenate([sample(200000, seed=5), [2.0 ** 20, 3.5e6, 2.0 ** 40, 1e300]])
+    s, c = twin_sincos(twin, x)
+    sn, cn = twin_sincos(twin, -x)
+    assert np.array_equal((-s).view(np.int64), sn.view(np.int64))
+    assert np.array_equal(c.view(np.int64), cn.view(np.int64))
