@@ -178,9 +178,11 @@ template <int S>
 __device__ __forceinline__ IncVals inc_vals(const double* tab, const int4 m, double4 c,
                                             const double th_i, const double u,
                                             const double th_j, const double w,
-                                            const int32_t out_l) {
+                                            const int32_t out_l, const bool ochk = true) {
     constexpr bool BATCH = S > 1;
-    if (BATCH) {  // outaged branch in some lane's scenario: rare, so test warp-wide first
+    // outaged branch in some lane's scenario: rare, so test warp-wide first
+    // (ochk: a warp-uniform pre-test per bus, see k_eval_staged)
+    if (BATCH && ochk) {
         const bool hit = m.y == out_l;
         if (__any_sync(__activemask(), hit) && hit) c = make_double4(0.0, 0.0, 0.0, 0.0);
     }
@@ -333,7 +335,8 @@ template <int MODE, int S, class Src, class JW>
 __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, const double* tab,
                                                            const int32_t i, const Src& src,
                                                            const Scen<S>& A, const int32_t ln,
-                                                           const int32_t out_l, const JW& jw) {
+                                                           const int32_t out_l, const JW& jw,
+                                                           const bool ochk = true) {
     const int32_t N = d.N;
     const int4 br = src.hdr0();
     const int4 rng = src.hdr1();
@@ -360,7 +363,7 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
         }
     } else {
         auto inc_step = [&](const int4 m, const double4 c, const double tj, const double wj) {
-            const IncVals v = inc_vals<S>(tab, m, c, th_i, v_i, tj, wj, out_l);
+            const IncVals v = inc_vals<S>(tab, m, c, th_i, v_i, tj, wj, out_l, ochk);
             inc_fold<MODE>(v, acc_p, acc_q, d_pt, d_pv, d_qt, d_qv);
             if (MODE & JAC) inc_offdiag(v, m, jw, rp, rq, nb);
         };
@@ -732,7 +735,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         }
         nrm = 0;
     };
-    int32_t out_l = -1;
+    int32_t out_l = -1, out_h = -1, out_k = -1;   // lane's outaged branch and its buses
     // prologue: item 0's copies in flight, item 1's record in a register
     issue(blockIdx.x, rec_word(blockIdx.x), slots_u32);
     int32_t rw_next = rec_word(blockIdx.x + stride);
@@ -754,6 +757,8 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             }
             const int32_t s = blk * PF_LANES + lane;
             out_l = (outage && s < K) ? __ldg(outage + s) : -1;
+            out_h = out_l >= 0 ? __ldg(d.bus_h + out_l) : -1;
+            out_k = out_l >= 0 ? __ldg(d.bus_k + out_l) : -1;
             __syncwarp();
         }
         unsigned char* sb = slots + (k & 1) * WS_SLOT_BYTES;
@@ -765,14 +770,17 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         cp_async_wait<1>();   // this item's group has landed (own lanes)
         __syncwarp();         // ... and every lane's
         const int32_t slot = grp * W + warp;
+        const int4* pk = reinterpret_cast<const int4*>(sb + WS_ROWS * WS_ROW_BYTES);
+        const int4 cnt = pk[2];
+        // does any lane's outaged branch end at this bus?  (usually not: then
+        // the per-incidence outage test is skipped)
+        const bool ochk = __any_sync(0xffffffffu, slot < d.N && (cnt.z == out_h || cnt.z == out_k));
         if (slot < d.N && blk * PF_LANES + lane < K) {
-            const int4* pk = reinterpret_cast<const int4*>(sb + WS_ROWS * WS_ROW_BYTES);
-            const int4 cnt = pk[2];
             const StagedSrc src{{d, A, A.y + lane, cnt.z, lane},
                                 reinterpret_cast<const double*>(sb) + lane, pk, cnt.x, cnt.y};
             nrm = max(nrm, eval_bus_src<MODE, PF_LANES>(
                                d, tab, cnt.z, src, A, lane, out_l,
-                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}));
+                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk));
         }
         __syncwarp();         // slot reads done before it is refilled
     }
@@ -1392,8 +1400,12 @@ static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const dou
 
 // Staged kernel shape: 12 warps per CTA, 2 CTAs per SM (24 warps at <= 80
 // registers), two 4 KB slots per warp (96 KB of shared memory per CTA).
-constexpr int WS_W = 12;
-constexpr int WS_MINB = 2;
+#ifndef PF_WS_W
+#define PF_WS_W 12
+#define PF_WS_MINB 2
+#endif
+constexpr int WS_W = PF_WS_W;
+constexpr int WS_MINB = PF_WS_MINB;
 constexpr size_t WS_SMEM = (size_t)WS_W * 2 * WS_SLOT_BYTES;
 template <int MODE>
 static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const double* y,

@@ -53,7 +53,10 @@ static_assert(SG_CAP_BUS <= SG_FIELD_MASK + 1 && SG_CAP_DUP <= SG_FIELD_MASK + 1
 // incidence t < ni, 2+2ni+2u / 3+2ni+2u operands a / b of staged device u < nv.
 // Row code = (array << 29) | entry (array 0 y, 1 pq_p, 2 pq_q, 3 pv_p), -1 none.
 // Incidences and devices past the staged ones are read from global memory.
-constexpr int WS_ROWS = 14;
+#ifndef PF_WS_ROWS
+#define PF_WS_ROWS 14
+#endif
+constexpr int WS_ROWS = PF_WS_ROWS;
 constexpr int WS_MAXINC = 6;
 constexpr int WS_MAXDEV = 2;
 constexpr int WS_PKT_UNITS = 3 + 3 * WS_MAXINC + 2 * WS_MAXDEV;   // 25
