@@ -333,7 +333,7 @@ def run_gpu(args):
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "bytes_per_scenario": per_scen, "static_bytes": static,
-                         "kernel_ms": kern_avg, "kernel": "k_eval_batched<RES|JAC|NORM>"},
+                         "kernel_ms": kern_avg, "kernel": "k_eval_staged<RES|JAC|NORM>"},
             "e2e": ({"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": bi,
                      "d2h_bytes_per_step": bo,
                      "api": "pf_eval_batched_host (pinned host buffers)", "steps": e2e_steps}
