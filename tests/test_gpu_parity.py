@@ -247,6 +247,30 @@ def test_batched_k1_without_outage_equals_single():
     assert float(nrm[0]) == n1
 
 
+def test_batched_perturbed_states_equal_single_evaluations():
+    """Config-1 style: 100 perturbed states of one grid in one batched launch
+    (base loads, no outages, K not a multiple of 32) equal 100 single-grid
+    evaluations bit for bit (bench.py's batch100 leg)."""
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    s = build_system(synth.config_case(1, seed=1))
+    plan = _plan(s)
+    ys = synth.perturbed_states(random_state(s, 7), s.n_bus, 100, seed=8)
+    K = len(ys)
+    g = plan.empty(plan.n_var, K)
+    j = plan.empty(plan.nnz, K)
+    nrm = plan.empty(K)
+    plan.eval_batched(K, _dev(to_blocked(ys)), g=g, jval=j, norms=nrm)
+    torch.cuda.synchronize()
+    G = from_blocked(g.cpu().numpy(), K, plan.n_var)
+    J = from_blocked(j.cpu().numpy(), K, plan.nnz)
+    for k in range(0, K, 7):
+        g1, j1, n1 = _eval(plan, ys[k])
+        assert np.array_equal(G[k], g1), k
+        assert np.array_equal(J[k], j1), k
+        assert float(nrm[k]) == n1
+
+
 def test_stress_hubs_config4_shape():
     """Config-4 generator (hubs of degree ~50) at reduced size; all
     scenarios vs oracle.  Full-size config 4 runs in the bench."""
