@@ -594,45 +594,65 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 constexpr int WS_ROW_BYTES = PF_LANES * 8;
 constexpr int WS_SLOT_BYTES = WS_ROWS * WS_ROW_BYTES + 32 * 16;   // rows + packet
 
-// Operand source reading a staged slot (rows + packet in shared memory):
-// the first ni incidences and nv devices of the bus; the rest (and the
-// parallel-branch re-reads) go through the global-memory accessors.
+// Operand source reading a staged slot (rows + packet in shared memory,
+// addressed through 32-bit shared-window addresses): the first ni incidences
+// and nv devices of the bus; the rest (and the parallel-branch re-reads) go
+// through the global-memory accessors.
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_v2f64(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds_v4s32(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a));
+    return v;
+}
+
 struct StagedSrc : GlobalSrc<PF_LANES> {
     static constexpr bool kStaged = true;
-    const double* rw;   // slot rows + lane: row r entry at rw[r * PF_LANES]
-    const int4* pk;     // slot packet
+    uint32_t rw;   // shared address of this lane's entry of row 0 (row r at + r * 256)
+    uint32_t pk;   // shared address of the slot packet
     int32_t ni, nv;
-    __device__ __forceinline__ int4 hdr0() const { return pk[0]; }
-    __device__ __forceinline__ int4 hdr1() const { return pk[1]; }
-    __device__ __forceinline__ double th_i() const { return rw[0]; }
-    __device__ __forceinline__ double v_i() const { return rw[PF_LANES]; }
+    __device__ __forceinline__ double row(int32_t r) const { return lds_f64(rw + r * WS_ROW_BYTES); }
+    __device__ __forceinline__ int4 hdr0() const { return lds_v4s32(pk); }
+    __device__ __forceinline__ int4 hdr1() const { return lds_v4s32(pk + 16); }
+    __device__ __forceinline__ double th_i() const { return row(0); }
+    __device__ __forceinline__ double v_i() const { return row(1); }
     __device__ __forceinline__ int32_t n_inc_staged() const { return ni; }
     __device__ __forceinline__ int32_t n_dev_staged() const { return nv; }
-    __device__ __forceinline__ int4 smeta(int32_t t) const { return pk[3 + t]; }
+    __device__ __forceinline__ int4 smeta(int32_t t) const { return lds_v4s32(pk + 16 * (3 + t)); }
     __device__ __forceinline__ double4 scoef(int32_t t) const {
-        const double2* c = reinterpret_cast<const double2*>(pk + 3 + ni + 2 * t);
-        const double2 a = c[0], b = c[1];
+        const uint32_t c = pk + 16 * (3 + ni + 2 * t);
+        const double2 a = lds_v2f64(c), b = lds_v2f64(c + 16);
         return make_double4(a.x, a.y, b.x, b.y);
     }
-    __device__ __forceinline__ double sth(int32_t t) const { return rw[(2 + 2 * t) * PF_LANES]; }
-    __device__ __forceinline__ double sv(int32_t t) const { return rw[(3 + 2 * t) * PF_LANES]; }
-    __device__ __forceinline__ int4 sdev(int32_t u) const { return pk[3 + 3 * ni + u]; }
+    __device__ __forceinline__ double sth(int32_t t) const { return row(2 + 2 * t); }
+    __device__ __forceinline__ double sv(int32_t t) const { return row(3 + 2 * t); }
+    __device__ __forceinline__ int4 sdev(int32_t u) const {
+        return lds_v4s32(pk + 16 * (3 + 3 * ni + u));
+    }
     __device__ __forceinline__ double2 scd(int32_t u) const {
-        return reinterpret_cast<const double2*>(pk + 3 + 3 * ni + nv)[u];
+        return lds_v2f64(pk + 16 * (3 + 3 * ni + nv + u));
     }
     // rows a / b: PQ (pq_p, pq_q), PV (pv_p, Q_g), Slack (P_s, Q_g); a scenario
     // array the caller did not pass falls back to the plan constants
     // (packet: PQ {p0, q0}, PV {v0, p0}, Slack {v0, theta0}, Shunt {g, b})
     __device__ __forceinline__ double sdev_a(const int4 dv, int32_t u) const {
-        const double r = rw[(2 + 2 * ni + 2 * u) * PF_LANES];
-        if (dv.x == DEV_PQ) return A.pq_p ? r : scd(u).x;
-        if (dv.x == DEV_PV) return A.pv_p ? r : scd(u).y;
-        return r;
+        if (dv.x == DEV_PQ && !A.pq_p) return scd(u).x;
+        if (dv.x == DEV_PV && !A.pv_p) return scd(u).y;
+        return row(2 + 2 * ni + 2 * u);
     }
     __device__ __forceinline__ double sdev_b(const int4 dv, int32_t u) const {
-        const double r = rw[(3 + 2 * ni + 2 * u) * PF_LANES];
-        if (dv.x == DEV_PQ) return A.pq_q ? r : scd(u).y;
-        return r;
+        if (dv.x == DEV_PQ && !A.pq_q) return scd(u).y;
+        return row(3 + 2 * ni + 2 * u);
     }
     __device__ __forceinline__ double sdev_c(int32_t u) const { return scd(u).x; }
     __device__ __forceinline__ double sdev_d(int32_t u) const { return scd(u).y; }
@@ -653,17 +673,15 @@ __device__ __forceinline__ void cp_async_wait() {
 // lane, the rows 16 lanes per row (two rows per instruction).  One commit
 // group per item.
 __device__ __forceinline__ void stage_item(const uint32_t sb, const int32_t rw,
-                                           const int4* __restrict__ pkt, const double* b0,
-                                           const double* b1, const double* b2, const double* b3,
-                                           const int lane) {
+                                           const int4* __restrict__ pkt,
+                                           const double* const* base, const int lane) {
     const int32_t off = __shfl_sync(0xffffffffu, rw, 14);
     const int32_t meta = __shfl_sync(0xffffffffu, rw, 15);
     const int32_t units = meta & 0xffff, rows = meta >> 16;
     if (lane < units) cp_async16(sb + WS_ROWS * WS_ROW_BYTES + lane * 16, pkt + off + lane);
     const double* src = nullptr;
     if (lane < rows && rw >= 0) {
-        const uint32_t arr = (uint32_t)rw >> 29;
-        const double* bp = arr == 0 ? b0 : arr == 1 ? b1 : arr == 2 ? b2 : b3;
+        const double* bp = base[(uint32_t)rw >> 29];
         if (bp) src = bp + (int64_t)(rw & 0x1fffffff) * PF_LANES;
     }
     const int half = lane >> 4, chunk = lane & 15;
@@ -710,13 +728,26 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         return __ldg(reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
                      ((lane + 2) & 15));
     };
+    // base pointers (y, pq_p, pq_q, pv_p) of the block being staged, per
+    // warp in shared memory, refreshed when the staged block changes
+    __shared__ const double* s_base[W][4];
+    __shared__ int32_t s_sblk[W];
+    if (lane == 0) s_sblk[warp] = -1;
+    __syncwarp();
     auto issue = [&](int32_t it, int32_t rw, uint32_t sb) {
         if (it < n_items && __shfl_sync(0xffffffffu, rw, 14) >= 0) {
-            const int64_t bb = blk_of(it);
-            stage_item(sb, rw, d.ws_pkt, y + bb * d.n_var * PF_LANES,
-                       pq_p ? pq_p + bb * d.P * PF_LANES : nullptr,
-                       pq_q ? pq_q + bb * d.P * PF_LANES : nullptr,
-                       pv_p ? pv_p + bb * d.G * PF_LANES : nullptr, lane);
+            const int32_t bb = blk_of(it);
+            if (bb != s_sblk[warp]) {
+                __syncwarp();
+                if (lane == 0) s_sblk[warp] = bb;
+                if (lane < 4) {
+                    const double* a = lane == 0 ? y : lane == 1 ? pq_p : lane == 2 ? pq_q : pv_p;
+                    const int64_t n = lane == 0 ? d.n_var : lane == 3 ? d.G : d.P;
+                    s_base[warp][lane] = a ? a + (int64_t)bb * n * PF_LANES : nullptr;
+                }
+                __syncwarp();
+            }
+            stage_item(sb, rw, d.ws_pkt, s_base[warp], lane);
         } else {
             cp_async_commit();   // keep one group per item
         }
@@ -776,8 +807,9 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         // the per-incidence outage test is skipped)
         const bool ochk = __any_sync(0xffffffffu, slot < d.N && (cnt.z == out_h || cnt.z == out_k));
         if (slot < d.N && blk * PF_LANES + lane < K) {
-            const StagedSrc src{{d, A, A.y + lane, cnt.z, lane},
-                                reinterpret_cast<const double*>(sb) + lane, pk, cnt.x, cnt.y};
+            const uint32_t sbu = slots_u32 + (k & 1) * WS_SLOT_BYTES;
+            const StagedSrc src{{d, A, A.y + lane, cnt.z, lane}, sbu + lane * 8,
+                                sbu + WS_ROWS * WS_ROW_BYTES, cnt.x, cnt.y};
             nrm = max(nrm, eval_bus_src<MODE, PF_LANES>(
                                d, tab, cnt.z, src, A, lane, out_l,
                                GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk));
