@@ -535,6 +535,45 @@ def test_single_grid_chunk_caps_vs_oracle():
         assert np.array_equal(jj[: plan.nnz].cpu().numpy(), j)
 
 
+def test_batched_staging_caps_vs_oracle():
+    """The staged batched kernel's caps (pf_internal.cuh WS_*): buses with more
+    than two devices (bus 25: six generators), more than six incidences (a
+    degree-350 hub), 40 parallel branches whose repeats straddle the staged /
+    global boundary, shunts, taps and shifts; with and without per-scenario
+    load arrays.  Every scenario against the oracle."""
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    s = build_system(_chunking_case())
+    plan = _plan(s)
+    o = oracle.Oracle(s)
+    _, _, perm = plan.pattern_csc()
+    K = 37
+    sb = synth.make_scenarios(s, K, seed=11)
+    t = lambda a: _dev(to_blocked(a))
+    outage = torch.as_tensor(sb.outage, device="cuda")
+    gr, jr, _ = o.eval_scenarios(K, to_blocked(sb.y.T), to_blocked(sb.pq_p.T),
+                                 to_blocked(sb.pq_q.T), to_blocked(sb.pv_p.T), sb.outage,
+                                 nthreads=4)
+    gb, jb, nr = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K), plan.empty(K)
+    plan.eval_batched(K, t(sb.y.T), t(sb.pq_p.T), t(sb.pq_q.T), t(sb.pv_p.T), outage, gb, jb, nr)
+    torch.cuda.synchronize()
+    G = from_blocked(gb.cpu().numpy(), K, plan.n_var)
+    J = from_blocked(jb.cpu().numpy(), K, plan.nnz)
+    assert_parity(G, from_blocked(gr, K, plan.n_var), "batched g")
+    assert_parity(J[:, perm], from_blocked(jr, K, plan.nnz), "batched J")
+    assert np.array_equal(nr[:K].cpu().numpy(), np.abs(G).max(axis=1))
+    # base loads (no per-scenario arrays), no outages: each scenario equals a
+    # single-grid evaluation of its state bit for bit
+    plan.eval_batched(K, t(sb.y.T), g=gb, jval=jb, norms=nr)
+    torch.cuda.synchronize()
+    G = from_blocked(gb.cpu().numpy(), K, plan.n_var)
+    J = from_blocked(jb.cpu().numpy(), K, plan.nnz)
+    for k in range(0, K, 6):
+        g1, j1, n1 = _eval(plan, sb.y[:, k])
+        assert np.array_equal(G[k], g1) and np.array_equal(J[k], j1), k
+        assert float(nr[k]) == n1
+
+
 def test_single_grid_back_to_back_and_produced_inputs():
     """Evaluations queued back to back (programmatic dependent launch lets
     the next one start early), each on a state that a torch kernel produced
