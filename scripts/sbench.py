@@ -26,9 +26,12 @@ for cfg in (int(a) for a in (sys.argv[1:] or ["2"])):
             plan.eval(ys[0], g, j, n)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
+    import os
+    mode = os.environ.get("MODE", "fjn")   # which outputs: f (g), j (J), n (norm)
     with torch.cuda.graph(graph, stream=st):
         for k in range(100):
-            plan.eval(ys[k], g, j, norms[k:k + 1])
+            plan.eval(ys[k], g if "f" in mode else None, j if "j" in mode else None,
+                      norms[k:k + 1] if "n" in mode else None)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     ts = []
     for _ in range(10):
@@ -39,5 +42,5 @@ for cfg in (int(a) for a in (sys.argv[1:] or ["2"])):
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 10)   # us per evaluation
-    print(f"config {cfg}: n_var {plan.n_var} nnz {plan.nnz}  graph {statistics.median(ts):.2f} "
+    print(f"[{mode}] config {cfg}: n_var {plan.n_var} nnz {plan.nnz}  graph {statistics.median(ts):.2f} "
           f"us/eval (100 states, min {min(ts):.2f})")
