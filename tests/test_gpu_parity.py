@@ -6,6 +6,8 @@ reference's; residual and Jacobian values per entry within
 max(1e-12 |ref|, 1e-14).
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -824,3 +826,44 @@ def test_device_batched_sparse_lu_vs_scipy():
         if k < 2:
             x_np = BL.reference_factor_solve(sched, J[k], -G[k])
             assert np.abs(X[k] - x_np).max() <= 1e-10 * max(1.0, np.abs(ref).max())
+
+
+def test_previous_batched_kernel_still_matches(tmp_path):
+    """PF_BATCHED_KERNEL=old selects the previous single-role batched kernel
+    (kept for A/B timing, scripts/ab_env.sh); in a fresh process it must give
+    the same bits as the staged product kernel."""
+    import subprocess
+    import sys
+
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2011_11880_b200 import synth
+from paper_2011_11880_b200.plan import Plan, to_blocked
+from paper_2011_11880_b200.system_model import build_system
+s = build_system(synth.synth_case(3000, 4200, seed=4, pq_frac=0.6, pv_frac=0.15,
+                                  shunt_frac=0.1, shift_frac=0.1, hub_frac=0.01, hub_degree=30))
+plan = Plan(s)
+K = 45
+sb = synth.make_scenarios(s, K, seed=3)
+t = lambda a: torch.as_tensor(to_blocked(a), device="cuda")
+g, j, n = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K), plan.empty(K)
+plan.eval_batched(K, t(sb.y.T), t(sb.pq_p.T), t(sb.pq_q.T), t(sb.pv_p.T),
+                  torch.as_tensor(sb.outage, device="cuda"), g, j, n)
+torch.cuda.synchronize()
+np.savez(sys.argv[2], g=g.cpu().numpy(), j=j.cpu().numpy(), n=n.cpu().numpy())
+"""
+    import os
+
+    root = str(Path(__file__).resolve().parents[1])
+    outs = {}
+    for kind in ("staged", "old"):
+        env = dict(os.environ)
+        env.pop("PF_BATCHED_KERNEL", None)
+        if kind == "old":
+            env["PF_BATCHED_KERNEL"] = "old"
+        f = tmp_path / f"{kind}.npz"
+        subprocess.run([sys.executable, "-c", code, root, str(f)], check=True, env=env)
+        outs[kind] = np.load(f)
+    for k in ("g", "j", "n"):
+        assert np.array_equal(outs["staged"][k], outs["old"][k]), k
