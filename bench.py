@@ -480,6 +480,24 @@ def _single_grid_config(dev, cfg: int, steps: int, cpu: bool = True) -> dict:
             if k >= 3:
                 bat.append(a.elapsed_time(b) / 100)
     torch.cuda.synchronize(dev)
+    # drop-in: the reference-facing host API a pflow caller uses (numpy y in,
+    # numpy g and the scipy CSC matrix out, pflow/newton.py:70 and :97):
+    # ResidualWorkspace.run + JacobianWorkspace.run, each a pf_eval_host call
+    from paper_2011_11880_b200.jacobian import JacobianWorkspace
+    from paper_2011_11880_b200.residual import ResidualWorkspace
+
+    rws, jws = ResidualWorkspace(s, plan), JacobianWorkspace(s, plan)
+    y_h = np.array(y0)
+    g_h = np.empty(plan.n_var)
+    rws.bind(y_h, g_h)
+    drop = []
+    for k in range(3 + max(steps, 10)):
+        t0 = time.perf_counter()
+        rws.run(y_h)
+        jws.run(y_h)
+        if k >= 3:
+            drop.append(time.perf_counter() - t0)
+    med_d = statistics.median(drop)
     # per state: y, g, J, norm; the plan's static data once per launch
     bytes_b = 100 * (16 * s.n_var + 8 * plan.nnz + 8) + static + 16 * len(s.pq) + 8 * len(s.pv)
     med_b = statistics.median(bat)
@@ -493,6 +511,9 @@ def _single_grid_config(dev, cfg: int, steps: int, cpu: bool = True) -> dict:
             "algorithmic_bytes": bytes_eval,
             "cold_frac": bytes_eval / (med_c / 1e3) / 1e9 / peak,
             "graph100_frac": bytes_eval / (med_g / 1e3) / 1e9 / peak,
+            "dropin_us_per_eval": med_d * 1e6, "dropin_evals_per_s": 1.0 / med_d,
+            "dropin_api": "ResidualWorkspace.run + JacobianWorkspace.run (numpy y, numpy g, "
+                          "scipy CSC J; host copies included)",
             "batch100_us_per_eval": med_b * 1e3, "batch100_evals_per_s": 1e3 / med_b,
             "batch100_frac": bytes_b / (med_b * 100 / 1e3) / 1e9 / peak,
             "batch100_kernel": "k_eval_staged<RES|JAC|NORM> (K = 100 states, one launch)",

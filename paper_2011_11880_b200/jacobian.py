@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 import scipy.sparse as sp
 
-from .plan import Plan
+from .plan import Plan, pinned_zeros
 from .residual import ResidualWorkspace, evaluate_residual
 
 
@@ -26,7 +26,12 @@ class JacobianWorkspace:
         n = self.plan.n_var
         indptr, indices, perm = self.plan.pattern_csc()
         self.nnz = self.plan.nnz
-        self.csc = sp.csc_matrix((np.zeros(self.nnz), indices, indptr), shape=(n, n))
+        # the values live in page-locked host memory, so each refresh is one
+        # DMA at full PCIe rate instead of a staged pageable copy
+        self._pinned, data = pinned_zeros(self.nnz)
+        self.csc = sp.csc_matrix((data, indices, indptr), shape=(n, n))
+        if not np.shares_memory(self.csc.data, data):
+            self.csc.data = data
         self.csc_perm = perm
         self._bound = None
 

@@ -29,6 +29,18 @@ def _stream_ptr(stream) -> int:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def pinned_zeros(n: int):
+    """(owner, array): a zeroed float64 numpy array of n entries in
+    page-locked host memory when CUDA is available (pageable otherwise);
+    keep ``owner`` alive as long as the array is used."""
+    torch = _torch()
+    if torch.cuda.is_available():
+        t = torch.zeros(max(n, 1), dtype=torch.float64, pin_memory=True)
+        return t, t.numpy()[:n]
+    a = np.zeros(n)
+    return a, a
+
+
 def n_blocks(K: int) -> int:
     return -(-int(K) // PF_LANES)
 

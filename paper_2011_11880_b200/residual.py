@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .plan import Plan
+from .plan import Plan, pinned_zeros
 
 
 class ResidualWorkspace:
@@ -26,7 +26,7 @@ class ResidualWorkspace:
         self.sys = sys
         self.plan = plan if plan is not None else Plan(sys)
         self.n_eq = self.plan.n_eq
-        self.residual = np.zeros(self.n_eq)
+        self._pinned, self.residual = pinned_zeros(self.n_eq)   # page-locked: one DMA per run
         self._bound = None
         self._out = None
 
