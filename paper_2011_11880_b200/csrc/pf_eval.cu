@@ -567,23 +567,23 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
     if (cur >= 0) flush(cur);
 }
 
-// ---- warp-specialised batched kernel ----------------------------------------
+// ---- staged batched kernel (the product batched path) ----------------------
 //
-// k_eval_staged: the product batched path.  Same items, order and arithmetic
-// as k_eval_batched (one warp = one bus x 32 scenarios), but the operands of
-// each item reach the evaluating warp through shared memory: one producer
-// warp per CTA walks the CTA's items ahead of the C consumer warps and, for
-// each, copies the bus's packet (header, incidence and device records,
-// device constants) and its scenario rows (own state, neighbour states,
-// device operands: 256 B each) into that consumer's ring slot with cp.async
-// (16 B per lane, two rows per warp instruction), then arms the slot's
-// "full" mbarrier with cp.async.mbarrier.arrive.  The consumer waits on it,
-// evaluates from shared memory and releases the slot on its "empty"
-// mbarrier.  The dependent global loads of the old kernel's per-item chain
-// (header -> records -> neighbour rows -> device rows) leave the consumers'
-// critical path: they overlap the previous item's arithmetic.  Incidences
-// and devices past the staged ones (plan caps WS_*) are read from global
-// memory as before.
+// k_eval_staged: same items, order and arithmetic as k_eval_batched (one
+// warp = one bus x 32 scenarios), but the operands of each item reach the
+// evaluating warp through shared memory.  Every warp owns two 4 KB slots.
+// While it evaluates item k from one slot, its cp.async copies of item k+1
+// fill the other: the bus's packet (header, incidence and device records,
+// device constants; plan-built, see pf_internal.cuh WS_ROWS) and its 256-byte
+// scenario rows (own state, neighbour states, device operands), 16 B per
+// lane and two rows per warp instruction, named by a 64-byte stage record
+// that was loaded one item earlier still.  The dependent global loads of the
+// old kernel's per-item chain (header -> records -> neighbour rows -> device
+// rows) thus overlap the previous item's arithmetic.  Warps stay independent:
+// no producer warp, no CTA barrier after the prologue (a producer-warp
+// version with an mbarrier ring measured 1.23 ms against 0.79 for this
+// scheme at the same stage of development).  Incidences and devices past
+// the staged ones are read from global memory as before.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
