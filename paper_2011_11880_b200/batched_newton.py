@@ -300,13 +300,98 @@ class BatchedLU:
 def _host_solve(plan, K, j, g, sc, indptr, indices):
     """Scenario ``sc``'s Newton step on the host with SuperLU (own pivoting);
     None when its Jacobian is singular."""
+    return _host_solves(plan, j, g, [sc], indptr, indices)[0]
+
+
+def _host_solves(plan, j, g, scs, indptr, indices):
+    """SuperLU steps of several scenarios, one host thread each (SuperLU
+    runs without the GIL); None where the Jacobian is singular."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
     n, nnz = plan.n_var, plan.nnz
-    jv = j.view(-1, nnz, PF_LANES)[sc // PF_LANES, :, sc % PF_LANES].cpu().numpy()
-    gv = g.view(-1, n, PF_LANES)[sc // PF_LANES, :, sc % PF_LANES].cpu().numpy()
+    sc_t = torch.as_tensor(np.asarray(scs, dtype=np.int64), device=j.device)
+    jv = j.view(-1, nnz, PF_LANES)[sc_t // PF_LANES, :, sc_t % PF_LANES].cpu().numpy()
+    gv = g.view(-1, n, PF_LANES)[sc_t // PF_LANES, :, sc_t % PF_LANES].cpu().numpy()
+
+    def one(i):
+        try:
+            a = sp.csr_matrix((jv[i], indices, indptr), shape=(n, n)).tocsc()
+            return spla.splu(a).solve(-gv[i])
+        except RuntimeError:
+            return None
+
+    if len(scs) == 1:
+        return [one(0)]
+    with ThreadPoolExecutor(max_workers=min(len(scs), os.cpu_count() or 1)) as ex:
+        return list(ex.map(one, range(len(scs))))
+
+
+# dense device fallback: largest system and the memory one chunk of dense
+# matrices may take
+_DENSE_MAX_N = 16384
+_DENSE_CHUNK_BYTES = 8 << 30
+_DENSE_PIVOT_RATIO = 1e-13   # below: near-singular, the host's SuperLU decides
+
+
+def _device_fallback(plan, j, g, scs, csr_rows, csr_cols):
+    """Newton steps of the scenarios ``scs`` whose shared-pivot solve failed.
+
+    A Jacobian with an exactly zero row or column is singular for any
+    pivoting, so SuperLU raises on it as pflow's solve does: those are
+    reported singular without a host factorisation.  The others are
+    factorised densely on the device with partial pivoting (cuSOLVER getrf
+    through ``torch.linalg.lu_factor_ex``), in chunks that fit
+    ``_DENSE_CHUNK_BYTES``.  Returns (steps, singular, host): a dict
+    scenario -> dy (device tensor), the scenarios found singular, and those
+    left to the host (a zero pivot inside the dense factorisation, or a
+    system too large to densify)."""
+    import torch
+
+    n, nnz = plan.n_var, plan.nnz
+    sc_t = torch.as_tensor(np.asarray(scs, dtype=np.int64), device=j.device)
+    vals = j.view(-1, nnz, PF_LANES)[sc_t // PF_LANES, :, sc_t % PF_LANES]   # [m, nnz]
+    rhs = g.view(-1, n, PF_LANES)[sc_t // PF_LANES, :, sc_t % PF_LANES]      # [m, n]
+    nzv = (vals != 0).to(torch.int8)
+    m = len(scs)
+    col_any = torch.zeros((m, n), dtype=torch.int8, device=j.device)
+    row_any = torch.zeros((m, n), dtype=torch.int8, device=j.device)
+    col_any.scatter_reduce_(1, csr_cols[None, :].expand(m, -1), nzv, reduce="amax")
+    row_any.scatter_reduce_(1, csr_rows[None, :].expand(m, -1), nzv, reduce="amax")
+    zero_line = ((col_any == 0).any(1) | (row_any == 0).any(1)).cpu().numpy()
+    singular = [int(scs[i]) for i in range(m) if zero_line[i]]
+    rest = [i for i in range(m) if not zero_line[i]]
+    steps, host = {}, []
+    if n > _DENSE_MAX_N:
+        return steps, singular, [int(scs[i]) for i in rest]
+    chunk = max(1, _DENSE_CHUNK_BYTES // (8 * n * n))
+    prev = torch.backends.cuda.preferred_linalg_library()
+    torch.backends.cuda.preferred_linalg_library("cusolver")   # getrf per matrix, not MAGMA batched
     try:
-        return spla.splu(sp.csr_matrix((jv, indices, indptr), shape=(n, n)).tocsc()).solve(-gv)
-    except RuntimeError:
-        return None
+        for c0 in range(0, len(rest), chunk):
+            idx = torch.as_tensor(rest[c0:c0 + chunk], device=j.device)
+            mc = idx.numel()
+            dense = torch.zeros((mc, n, n), dtype=torch.float64, device=j.device)
+            bi = torch.arange(mc, device=j.device)[:, None]
+            dense[bi, csr_rows[None, :], csr_cols[None, :]] = vals[idx]
+            lu, piv, info = torch.linalg.lu_factor_ex(dense)
+            dx = torch.linalg.lu_solve(lu, piv, -rhs[idx][:, :, None])[:, :, 0]
+            # a pivot many orders below the largest: SuperLU (other pivots)
+            # may hit an exact zero there, so the host decides
+            du = lu.diagonal(dim1=1, dim2=2).abs()
+            ratio = (du.amin(1) / du.amax(1)).cpu().numpy()
+            info = info.cpu().numpy()
+            for k in range(mc):
+                sc = int(scs[rest[c0 + k]])
+                if info[k] == 0 and ratio[k] > _DENSE_PIVOT_RATIO:
+                    steps[sc] = dx[k]
+                else:
+                    host.append(sc)
+            del dense, lu
+    finally:
+        torch.backends.cuda.preferred_linalg_library(prev)
+    return steps, singular, host
 
 
 @dataclass
@@ -321,7 +406,7 @@ class BatchedResult:
 
 def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None, outage=None,
                          tol: float = 1e-8, max_iter: int = 20, lu: BatchedLU | None = None,
-                         linear: str = "device") -> BatchedResult:
+                         linear: str = "device", fallback: str = "device") -> BatchedResult:
     """Newton on K scenarios in place on the blocked state ``y`` (CUDA
     float64, plan layout).  Returns per-scenario outcomes; ``y`` holds each
     scenario's last iterate.
@@ -330,7 +415,14 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
     scenarios (batched_lu.py), with outage-proof pivots
     (``robust_row_match``); a singular scenario shows up as a non-finite
     mismatch and is reported diverged.  ``linear="cusolverrf"``: one
-    cusolverRf handle per scenario, each with its own pivoting."""
+    cusolverRf handle per scenario, each with its own pivoting.
+
+    A scenario whose shared-pivot solve fails its accuracy check is solved
+    with its own pivoting: ``fallback="device"`` (default) factorises it
+    densely on the device (``_device_fallback``; an exactly zero row or
+    column is reported singular, as pflow's SuperLU solve raises on it), and
+    only a zero pivot inside that factorisation goes to SuperLU on the host;
+    ``fallback="host"`` sends every such scenario to SuperLU."""
     import torch
 
     if tol <= 0 or max_iter < 1:
@@ -345,6 +437,8 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
     timings = {"eval": 0.0, "handoff": 0.0, "lu": 0.0, "update": 0.0, "setup": 0.0}
     if linear not in ("device", "cusolverrf"):
         raise ValueError("linear must be 'device' or 'cusolverrf'")
+    if fallback not in ("device", "host"):
+        raise ValueError("fallback must be 'device' or 'host'")
     dlu = None
     if linear == "device" and lu is None:
         # one schedule for every scenario: pivoting from scenario 0 at the
@@ -362,6 +456,9 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
         indptr_h, indices_h = indptr, indices
         csr_ptr = torch.as_tensor(indptr, dtype=torch.int32, device=dev)
         csr_idx = torch.as_tensor(indices, dtype=torch.int32, device=dev)
+        csr_idx_l = csr_idx.to(torch.int64)
+        csr_row = torch.repeat_interleave(torch.arange(n, device=dev),
+                                          torch.as_tensor(np.diff(indptr), device=dev))
         res = plan.empty(K)
         torch.cuda.synchronize(dev)
         timings["setup"] = time.perf_counter() - t0
@@ -378,7 +475,8 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
     conv = np.zeros(K, dtype=bool)
     div = np.zeros(K, dtype=bool)
     singular = np.zeros(K, dtype=bool)
-    host_solves = 0
+    host_solves = device_fallback = zero_line_singular = 0
+    host_only = np.zeros(K, dtype=bool)
     iters = np.zeros(K, dtype=np.int64)
     mism = np.full(K, np.inf)
     stream = torch.cuda.current_stream(dev).cuda_stream
@@ -411,15 +509,33 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
             ok = live & np.isfinite(rh) & (rh <= _LIN_RTOL * np.maximum(nh, 1e-300))
             active.copy_(torch.as_tensor(ok.astype(np.int32)))
             dlu.add(dx, y, active)
-            for sc in np.nonzero(live & ~ok)[0]:
-                dy = _host_solve(plan, K, j, g, int(sc), indptr_h, indices_h)
-                if dy is None:              # singular: pflow's solve raises here
+            failed = np.nonzero(live & ~ok)[0]
+            yv = y.view(-1, n, PF_LANES)
+            # a scenario that was near-singular once goes straight to the host
+            host_list = [int(sc) for sc in failed if host_only[sc]]
+            dev_try = np.array([sc for sc in failed if not host_only[sc]], dtype=np.int64)
+            if dev_try.size and fallback == "device":
+                steps, sing, more = _device_fallback(plan, j, g, dev_try, csr_row, csr_idx_l)
+                for sc in sing:             # exactly singular: pflow's solve raises here
                     singular[sc] = True
                     live[sc] = False
-                    continue
-                yv = y.view(-1, n, PF_LANES)
-                yv[sc // PF_LANES, :, sc % PF_LANES] += torch.as_tensor(dy, device=dev)
-                host_solves += 1
+                for sc, dy in steps.items():
+                    yv[sc // PF_LANES, :, sc % PF_LANES] += dy
+                host_only[more] = True
+                host_list += more
+                device_fallback += len(steps)
+                zero_line_singular += len(sing)
+            else:
+                host_list += [int(sc) for sc in dev_try]
+            if host_list:
+                for sc, dy in zip(host_list, _host_solves(plan, j, g, host_list, indptr_h,
+                                                          indices_h)):
+                    if dy is None:          # singular: pflow's solve raises here
+                        singular[sc] = True
+                        live[sc] = False
+                        continue
+                    yv[sc // PF_LANES, :, sc % PF_LANES] += torch.as_tensor(dy, device=dev)
+                    host_solves += 1
             iters[live] += 1
             torch.cuda.synchronize(dev)
             timings["update"] += time.perf_counter() - t0
@@ -444,5 +560,7 @@ def batched_newton_solve(plan: Plan, K: int, y, pq_p=None, pq_q=None, pv_p=None,
         timings["update"] += time.perf_counter() - t0
     torch.cuda.synchronize(dev)
     timings["host_fallback_solves"] = host_solves
+    timings["device_fallback_solves"] = device_fallback
+    timings["zero_line_singular"] = zero_line_singular
     return BatchedResult(converged=conv, diverged=div, iterations=iters, final_mismatch=mism,
                          singular=singular, timings=timings)

@@ -671,8 +671,9 @@ def _cpu_newton(o, y, pq_p, pq_q, pv_p, outage, tol=1e-8, max_iter=20):
         it += 1
 
 
-@pytest.mark.parametrize("linear", ["device", "cusolverrf"])
-def test_batched_newton_vs_cpu_newton(linear):
+@pytest.mark.parametrize("linear,fallback", [("device", "device"), ("device", "host"),
+                                             ("cusolverrf", "device")])
+def test_batched_newton_vs_cpu_newton(linear, fallback):
     """Device-resident batched Newton (pf_eval_batched + cusolverRf
     refactorisation on the fixed pattern) against pflow's loop restated on the
     CPU oracle with SuperLU, scenario by scenario: same outcome, same
@@ -692,7 +693,7 @@ def test_batched_newton_vs_cpu_newton(linear):
     t = lambda a: _dev(to_blocked(np.ascontiguousarray(a.T)))
     outage = torch.as_tensor(sb.outage, device="cuda")
     res = batched_newton_solve(plan, K, y_dev, t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), outage,
-                               linear=linear)
+                               linear=linear, fallback=fallback)
     Yg = from_blocked(y_dev.cpu().numpy(), K, plan.n_var)
     n_conv = 0
     for k in range(K):
@@ -706,6 +707,8 @@ def test_batched_newton_vs_cpu_newton(linear):
             assert res.final_mismatch[k] <= 1e-8
         else:
             assert not res.converged[k], (k, status)
+            if status == "singular":
+                assert res.singular[k], k
     assert n_conv >= K // 2
 
 
