@@ -72,26 +72,28 @@ PF_HD void pf_two_sum(double a, double b, double* s, double* e) {
 /* tab: PF_TRIG_N * 4 doubles {Sh, Ch, Sl, Cl} (pf_trig_tab, possibly staged
  * in shared memory by the caller). */
 PF_HD void pf_sincos_tab(double x, const double* tab, double* sp, double* cp) {
-    if (!(fabs(x) < 1048576.0)) {
-        /* evaluated at |x| so that, like the fast path, sin is odd and cos
-         * even bit for bit (the kernels evaluate one branch terminal at
-         * -thk, pf_eval.cu inc_terms) */
-#ifdef __CUDA_ARCH__
-        const double2 r = pf_sincos_slow(fabs(x));
-        *sp = x < 0.0 ? -r.x : r.x;
-        *cp = r.y;
-#else
-        *sp = x < 0.0 ? -sin(-x) : sin(x);
-        *cp = cos(fabs(x));
-#endif
-        return;
-    }
     /* 1. r = x - k pi/2 in double-double.  |x| <= pi/4 (the usual power-flow
      * angle difference) has k = 0, for which the reduction is the identity
-     * bit for bit, so it is skipped. */
+     * bit for bit, so it is skipped.  Everything else (NaN included) is
+     * tested further inside the rare branch, so the common path pays one
+     * comparison. */
     double kf = 0.0, rh = x, rl = 0.0;
-    const bool reduce = fabs(x) > 0.78539816339744828;
+    const bool reduce = !(fabs(x) <= 0.78539816339744828);
     if (reduce) {
+        if (!(fabs(x) < 1048576.0)) {
+            /* huge, infinite or NaN: evaluated at |x| so that, like the
+             * fast path, sin is odd and cos even bit for bit (the kernels
+             * evaluate one branch terminal at -thk, pf_eval.cu inc_terms) */
+#ifdef __CUDA_ARCH__
+            const double2 r = pf_sincos_slow(fabs(x));
+            *sp = x < 0.0 ? -r.x : r.x;
+            *cp = r.y;
+#else
+            *sp = x < 0.0 ? -sin(-x) : sin(x);
+            *cp = cos(fabs(x));
+#endif
+            return;
+        }
         kf = rint(x * PF_TWO_OVER_PI);
         const double ph = kf * PF_PIO2_1;
         const double pl = fma(kf, PF_PIO2_1, -ph);
