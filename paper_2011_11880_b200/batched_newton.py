@@ -303,29 +303,36 @@ def _host_solve(plan, K, j, g, sc, indptr, indices):
     return _host_solves(plan, j, g, [sc], indptr, indices)[0]
 
 
-def _host_solves(plan, j, g, scs, indptr, indices):
-    """SuperLU steps of several scenarios, one host thread each (SuperLU
-    runs without the GIL); None where the Jacobian is singular."""
-    from concurrent.futures import ThreadPoolExecutor
+_POOL = None
 
+
+def _pool():
+    """Worker processes for host SuperLU solves (spawned once, on first use)."""
+    global _POOL
+    if _POOL is None:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+
+        _POOL = ProcessPoolExecutor(max_workers=min(16, os.cpu_count() or 1),
+                                    mp_context=mp.get_context("spawn"))
+    return _POOL
+
+
+def _host_solves(plan, j, g, scs, indptr, indices):
+    """SuperLU steps of several scenarios, in parallel worker processes
+    (``_superlu``); None where the Jacobian is singular."""
     import torch
+
+    from . import _superlu
 
     n, nnz = plan.n_var, plan.nnz
     sc_t = torch.as_tensor(np.asarray(scs, dtype=np.int64), device=j.device)
     jv = j.view(-1, nnz, PF_LANES)[sc_t // PF_LANES, :, sc_t % PF_LANES].cpu().numpy()
     gv = g.view(-1, n, PF_LANES)[sc_t // PF_LANES, :, sc_t % PF_LANES].cpu().numpy()
-
-    def one(i):
-        try:
-            a = sp.csr_matrix((jv[i], indices, indptr), shape=(n, n)).tocsc()
-            return spla.splu(a).solve(-gv[i])
-        except RuntimeError:
-            return None
-
-    if len(scs) == 1:
-        return [one(0)]
-    with ThreadPoolExecutor(max_workers=min(len(scs), os.cpu_count() or 1)) as ex:
-        return list(ex.map(one, range(len(scs))))
+    jobs = [(jv[i], -gv[i], indptr, indices, n) for i in range(len(scs))]
+    if len(jobs) == 1 or (os.cpu_count() or 1) == 1:
+        return [_superlu.solve(a) for a in jobs]
+    return list(_pool().map(_superlu.solve, jobs))
 
 
 # dense device fallback: largest system and the memory one chunk of dense
