@@ -870,3 +870,46 @@ np.savez(sys.argv[2], g=g.cpu().numpy(), j=j.cpu().numpy(), n=n.cpu().numpy())
         outs[kind] = np.load(f)
     for k in ("g", "j", "n"):
         assert np.array_equal(outs["staged"][k], outs["old"][k]), k
+
+
+def test_newton_fallback_paths():
+    """The batched Newton's per-scenario fallbacks: the dense device LU solves
+    as SciPy does; an exactly zero Jacobian column (an isolated bus) is
+    reported singular, as SuperLU raises on it; the worker-process SuperLU
+    path returns SciPy's own solution and None for the singular one."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+
+    from paper_2011_11880_b200 import batched_newton as BN
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    s = build_system(_light_case(400, 520, seed=5))
+    plan = _plan(s)
+    K = 6
+    sb = synth.make_scenarios(s, K, seed=6, outages=False)
+    t = lambda a: _dev(to_blocked(np.ascontiguousarray(a.T)))
+    g, j = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K)
+    plan.eval_batched(K, t(sb.y), t(sb.pq_p), t(sb.pq_q), t(sb.pv_p), None, g, j, None)
+    indptr, indices = plan.pattern_csr()
+    n, nnz = plan.n_var, plan.nnz
+    # scenario 5: zero the theta column of bus 3 (every entry of column 3)
+    col = np.flatnonzero(indices == 3)
+    jv = j.view(-1, nnz, 32)
+    jv[0, torch.as_tensor(col, device="cuda"), 5] = 0.0
+    torch.cuda.synchronize()
+    J = from_blocked(j.cpu().numpy(), K, nnz)
+    G = from_blocked(g.cpu().numpy(), K, n)
+    rows = torch.repeat_interleave(torch.arange(n, device="cuda"),
+                                   torch.as_tensor(np.diff(indptr), device="cuda"))
+    cols = torch.as_tensor(indices, dtype=torch.int64, device="cuda")
+    steps, sing, host = BN._device_fallback(plan, j, g, np.arange(K), rows, cols)
+    assert sing == [5] and not host and sorted(steps) == [0, 1, 2, 3, 4]
+    for k in range(5):
+        A = sp.csr_matrix((J[k], indices, indptr), shape=(n, n)).tocsc()
+        ref = spla.spsolve(A, -G[k])
+        assert np.abs(steps[k].cpu().numpy() - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max())
+    host_steps = BN._host_solves(plan, j, g, [1, 5, 2], indptr, indices)
+    assert host_steps[1] is None
+    for k, hs in zip((1, 2), (host_steps[0], host_steps[2])):
+        A = sp.csr_matrix((J[k], indices, indptr), shape=(n, n)).tocsc()
+        assert np.array_equal(hs, spla.splu(A).solve(-G[k]))
