@@ -1430,14 +1430,8 @@ static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const dou
     return cudaSuccess;
 }
 
-// Staged kernel shape: 12 warps per CTA, 2 CTAs per SM (24 warps at <= 80
-// registers), two 4 KB slots per warp (96 KB of shared memory per CTA).
-#ifndef PF_WS_W
-#define PF_WS_W 12
-#define PF_WS_MINB 2
-#endif
-constexpr int WS_W = PF_WS_W;
-constexpr int WS_MINB = PF_WS_MINB;
+// Staged kernel shape (pf_internal.cuh WS_W, WS_MINB): two 4 KB slots per
+// warp in dynamic shared memory.
 constexpr size_t WS_SMEM = (size_t)WS_W * 2 * WS_SLOT_BYTES;
 template <int MODE>
 static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const double* y,

@@ -58,6 +58,18 @@ static_assert(SG_CAP_BUS <= SG_FIELD_MASK + 1 && SG_CAP_DUP <= SG_FIELD_MASK + 1
 #endif
 constexpr int WS_ROWS = PF_WS_ROWS;
 constexpr int WS_MAXINC = 6;
+// CTA shape: WS_W warps, WS_MINB CTAs per SM (24 warps/SM at 80 registers).
+// A CTA's item is a group of WS_W consecutive slots of the processing order.
+// Measured on B200 (ms per launch, config 3 / config 4): 24 x 1 0.597 /
+// 0.645 with hubs first in the order (0.61 with hubs spread, see
+// pf_plan.cu), 12 x 2 0.625 / 0.615, 20 x 1 (91 registers) 0.613 / 0.627,
+// 16 x 1 (104 registers) 0.662 / 0.636, 6 x 4 0.640 / 0.608.
+#ifndef PF_WS_W
+#define PF_WS_W 24
+#define PF_WS_MINB 1
+#endif
+constexpr int WS_W = PF_WS_W;
+constexpr int WS_MINB = PF_WS_MINB;
 constexpr int WS_MAXDEV = 2;
 constexpr int WS_PKT_UNITS = 3 + 3 * WS_MAXINC + 2 * WS_MAXDEV;   // 25
 constexpr int WS_REC_WORDS = 2 + WS_ROWS;                        // 16 (64 bytes)

@@ -601,15 +601,46 @@ int build(const pf_topology* t, pf_plan** out) {
     int32_t md = 0;
     for (int32_t i = 0; i < N; ++i) md = std::max(md, hptr[i + 1] - hptr[i]);
     P->max_deg = md;
-    // batched processing order: high-degree buses first, then the rest, each
-    // in bus order (the identity when there are no hubs)
+    // batched processing order (the identity when there are no hubs)
     std::vector<int32_t> order;
     {
-        order.reserve(N);
+        // Hubs go into the first rounds of the staged kernel's schedule,
+        // spread so that every CTA (hence every SM) and every warp gets at
+        // most one more than the others: CTA c processes groups c, c + G,
+        // ... of WS_W slots (G = resident CTAs), so hub h takes CTA h mod G,
+        // warp (h / G) mod WS_W, round h / (G WS_W).  Heaviest hubs first.
+        // Buses of ordinary degree fill the remaining slots in bus order.
+        std::vector<int32_t> hubs;
         for (int32_t i = 0; i < N; ++i)
-            if (hptr[i + 1] - hptr[i] >= HUB_DEG) order.push_back(i);
-        for (int32_t i = 0; i < N; ++i)
-            if (hptr[i + 1] - hptr[i] < HUB_DEG) order.push_back(i);
+            if (hptr[i + 1] - hptr[i] >= HUB_DEG) hubs.push_back(i);
+        std::stable_sort(hubs.begin(), hubs.end(), [&](int32_t a, int32_t b) {
+            return hptr[a + 1] - hptr[a] > hptr[b + 1] - hptr[b];
+        });
+        int dev = 0, sms = 0;
+        PF_TRY(cudaGetDevice(&dev));
+        PF_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int64_t n_groups = (N + WS_W - 1) / WS_W;
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * WS_MINB, n_groups));
+        order.assign(N, -1);
+        std::vector<char> taken((size_t)n_groups * WS_W, 0);
+        for (int64_t h = 0; h < (int64_t)hubs.size(); ++h) {
+            const int64_t c = h % G, w = (h / G) % WS_W, r = h / (G * WS_W);
+            int64_t slot = (r * G + c) * WS_W + w;
+            while (slot < N && taken[slot]) ++slot;   // (not reached for in-range rounds)
+            if (slot >= N) {                            // degenerate tiny grids
+                slot = 0;
+                while (taken[slot]) ++slot;
+            }
+            taken[slot] = 1;
+            order[slot] = hubs[h];
+        }
+        int32_t next = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            if (hptr[i + 1] - hptr[i] >= HUB_DEG) continue;
+            while (taken[next]) ++next;
+            taken[next] = 1;
+            order[next] = i;
+        }
         // (kept as a load even when it is the identity: measured faster on
         // B200 than a conditional bypass, 0.738 vs 0.776 ms at config 3)
         int32_t* bus_order;
