@@ -758,7 +758,16 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     // block (integer max of |g| bit patterns: exact, order-independent).  No
     // CTA barrier: warps cross block boundaries independently.
     int32_t cur = -1;
-    unsigned long long nrm = 0;
+    // per-lane state that is touched once per item lives in shared memory,
+    // leaving the registers to the evaluation (B200, config 3: 0.598 -> 0.593 ms)
+    __shared__ unsigned long long s_nrm[W][32];
+    __shared__ int32_t s_out[3][W][32];
+    unsigned long long& nrm = s_nrm[warp][lane];
+    int32_t& out_l = s_out[0][warp][lane];
+    int32_t& out_h = s_out[1][warp][lane];
+    int32_t& out_k = s_out[2][warp][lane];
+    nrm = 0;
+    out_l = out_h = out_k = -1;   // lane's outaged branch and its buses
     auto flush = [&](int32_t blk) {
         if (MODE & NORM) {
             const int32_t s = blk * PF_LANES + lane;
@@ -766,7 +775,6 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         }
         nrm = 0;
     };
-    int32_t out_l = -1, out_h = -1, out_k = -1;   // lane's outaged branch and its buses
     // prologue: item 0's copies in flight, item 1's record in a register
     issue(blockIdx.x, rec_word(blockIdx.x), slots_u32);
     int32_t rw_next = rec_word(blockIdx.x + stride);
