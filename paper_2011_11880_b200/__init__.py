@@ -40,7 +40,7 @@ def __getattr__(name):
 
         return getattr(jacobian, name)
     if name in ("NewtonOptions", "SolveResult", "newton_solve", "SingularMatrixError",
-                "SuperLUSolver"):
+                "SuperLUSolver", "QLimitResult", "newton_solve_q_limits"):
         from . import newton
 
         return getattr(newton, name)
@@ -60,7 +60,8 @@ __all__ = [
     "PowerSystem", "PqGroup", "PvGroup", "RawCase", "ResidualWorkspace", "ScenarioBuffers",
     "ShuntGroup", "SlackGroup", "SolveResult", "Violation", "build_system", "count_variables",
     "batched_newton_solve", "evaluate_jacobian", "evaluate_residual", "finite_difference_jacobian", "flat_start",
-    "from_rows", "gather_norms", "make_case", "newton_solve", "parse_case", "parse_case_file",
+    "from_rows", "gather_norms", "make_case", "newton_solve", "newton_solve_q_limits",
+    "QLimitResult", "parse_case", "parse_case_file",
     "random_state", "shard", "symbolic_pattern", "validate_case", "write_case",
     "SingularMatrixError", "SuperLUSolver", "WORKFLOW_TABLE", "IntraStrategy", "WorkflowConfig",
     "WorkflowConfigError", "all_workflows", "set_worker_count", "worker_count", "workflow_config",

@@ -913,3 +913,51 @@ def test_newton_fallback_paths():
     for k, hs in zip((1, 2), (host_steps[0], host_steps[2])):
         A = sp.csr_matrix((J[k], indices, indptr), shape=(n, n)).tocsc()
         assert np.array_equal(hs, spla.splu(A).solve(-G[k]))
+
+
+def test_q_limits_pv_to_pq_switching():
+    """PV -> PQ switching on reactive limits, an outer loop
+    around the GPU Newton.  pflow has no limits, so the checks are
+    self-consistency against the CPU oracle.  With loose limits nothing
+    switches and the result is the plain solve.  With one generator's qmax
+    below its free Q_g, that generator is fixed at qmax as PQ demand and its
+    bus voltage is released.  The other PV generators stay within limits,
+    and the final state solves the switched case (oracle residual)."""
+    from dataclasses import replace
+
+    from paper_2011_11880_b200.newton import (NewtonOptions, _pv_gen_rows, newton_solve,
+                                              newton_solve_q_limits)
+    from paper_2011_11880_b200.system_model import flat_start
+    from _util import case_of
+
+    raw = case_of(load("case14"))
+    loose = replace(raw, qmax=np.full(raw.n_gen, 1e4), qmin=np.full(raw.n_gen, -1e4))
+    out = newton_solve_q_limits(loose)
+    s0 = build_system(loose)
+    plain = newton_solve(s0, flat_start(s0), NewtonOptions())
+    assert out.switched == [] and out.rounds == 1
+    assert out.result.converged and np.array_equal(out.result.y, plain.y)
+
+    rows = _pv_gen_rows(loose)
+    q_free = plain.y[2 * s0.n_bus: 2 * s0.n_bus + len(rows)] * loose.base_mva
+    k = int(np.argmax(q_free))            # the PV gen with the largest Q_g
+    r = int(rows[k])
+    qmax = loose.qmax.copy()
+    qmax[r] = q_free[k] - 5.0
+    tight = replace(loose, qmax=qmax)
+    out = newton_solve_q_limits(tight)
+    assert out.result.converged and out.rounds >= 2
+    assert (r, "qmax", qmax[r]) in out.switched
+    sys_f = out.system
+    # the final state solves the switched case
+    o = oracle.Oracle(sys_f)
+    assert np.abs(o.residual(out.result.y)).max() <= 1e-8
+    # the switched gen is now fixed PQ demand -qmax; its bus voltage moved off vg
+    bus_pos = int(np.flatnonzero(tight.bus_id == tight.gen_bus[r])[0])
+    assert out.case.bus_type[bus_pos] == 1
+    assert out.case.qg[r] == qmax[r]
+    assert abs(out.result.y[sys_f.n_bus + bus_pos] - tight.vg[r]) > 1e-6
+    # every generator still PV is within its limits
+    rows_f = _pv_gen_rows(out.case)
+    q_f = out.result.y[2 * sys_f.n_bus: 2 * sys_f.n_bus + len(rows_f)] * tight.base_mva
+    assert np.all(q_f <= tight.qmax[rows_f] + 1e-9) and np.all(q_f >= tight.qmin[rows_f] - 1e-9)
