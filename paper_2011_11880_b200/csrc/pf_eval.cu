@@ -698,7 +698,7 @@ __device__ __forceinline__ void stage_item(const uint32_t sb, const int32_t rw,
 // coupling): at the start of item k it issues item k+1's copies into its
 // other slot and loads item k+2's stage record, then waits for item k's
 // copies (issued one item earlier) and evaluates from shared memory.
-template <int MODE, int W, int MINB>
+template <int MODE, int W, int MINB, bool DYN>
 __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     const DevicePlan d, const int32_t K, const int32_t n_groups, const int32_t n_items,
     const double* __restrict__ y, const double* __restrict__ pq_p,
@@ -708,22 +708,52 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     extern __shared__ __align__(128) unsigned char ws_smem[];
     __shared__ double s_tab[PF_TRIG_N * 4];
     __shared__ Scen<PF_LANES> As[W];   // per-warp block base pointers
-    const double* tab = stage_trig_table(s_tab);
+    __shared__ int32_t s_ctr;          // dynamic mode: next slot claim of this CTA
+    __shared__ int32_t s_total;        // dynamic mode: slots of this CTA
+    if (DYN && threadIdx.x == 0) {
+        s_ctr = 0;
+        s_total = (int32_t)blockIdx.x < n_items
+                      ? ((n_items - (int32_t)blockIdx.x + (int32_t)gridDim.x - 1) /
+                         (int32_t)gridDim.x) * W
+                      : 0;
+    }
+    const double* tab = stage_trig_table(s_tab);   // (its barrier publishes s_ctr, s_total)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Scen<PF_LANES>& A = As[warp];
     unsigned char* slots = ws_smem + (size_t)warp * 2 * WS_SLOT_BYTES;
     const uint32_t slots_u32 = smem_u32(slots);
 
-    // items are walked with a stride of gridDim.x; item -> (block, group)
-    // by multiply-shift division (fd_m, fd_l: n_groups), so the look-ahead
-    // costs no loop-carried registers.  The warp's bus slot is grp * W + warp.
+    // Work: the CTA owns items blockIdx.x, blockIdx.x + G, ... (G =
+    // gridDim.x), each a group of W consecutive bus slots; item -> (block,
+    // group) by multiply-shift division (fd_m, fd_l: n_groups).
+    //  * static (DYN = false): warp w takes slot w of each of the CTA's
+    //    items, so a step's item is blockIdx.x + k G;
+    //  * dynamic (DYN = true): the warps claim the CTA's slots in order from a
+    //    shared counter (q = local item * W + slot), so a warp held up by an
+    //    expensive bus (a hub with many incidences past the staged ones)
+    //    claims fewer and the load balances inside the CTA.  Claims run two
+    //    steps ahead (the staging pipeline) in a per-warp ring.
+    // A step is named by x: the item (static) or the claim q (dynamic).
     const int32_t stride = gridDim.x;
     auto blk_of = [&](int32_t it) -> int32_t {
         return (int32_t)((__umulhi((uint32_t)it, fd_m) + (uint32_t)it) >> fd_l);
     };
-    auto rec_word = [&](int32_t it) -> int32_t {
-        if (it >= n_items) return -1;
-        const int32_t slot = (it - blk_of(it) * n_groups) * W + warp;
+    auto item_of = [&](int32_t x) -> int32_t {
+        if constexpr (DYN) return (int32_t)blockIdx.x + (x / W) * stride;
+        else return x;
+    };
+    auto sub_of = [&](int32_t x) -> int32_t {
+        if constexpr (DYN) return x % W;
+        else return warp;
+    };
+    auto live = [&](int32_t x) -> bool {
+        if constexpr (DYN) return x < s_total;
+        else return x < n_items;
+    };
+    auto rec_word = [&](int32_t x) -> int32_t {
+        if (!live(x)) return -1;
+        const int32_t it = item_of(x);
+        const int32_t slot = (it - blk_of(it) * n_groups) * W + sub_of(x);
         if (slot >= d.N) return -1;
         return __ldg(reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
                      ((lane + 2) & 15));
@@ -734,9 +764,9 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     __shared__ int32_t s_sblk[W];
     if (lane == 0) s_sblk[warp] = -1;
     __syncwarp();
-    auto issue = [&](int32_t it, int32_t rw, uint32_t sb) {
-        if (it < n_items && __shfl_sync(0xffffffffu, rw, 14) >= 0) {
-            const int32_t bb = blk_of(it);
+    auto issue = [&](int32_t x, int32_t rw, uint32_t sb) {
+        if (live(x) && __shfl_sync(0xffffffffu, rw, 14) >= 0) {
+            const int32_t bb = blk_of(item_of(x));
             if (bb != s_sblk[warp]) {
                 __syncwarp();
                 if (lane == 0) s_sblk[warp] = bb;
@@ -749,25 +779,31 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             }
             stage_item(sb, rw, d.ws_pkt, s_base[warp], lane);
         } else {
-            cp_async_commit();   // keep one group per item
+            cp_async_commit();   // keep one group per step
         }
     };
 
     // norms: each warp keeps a per-lane running max over its items of the
-    // current scenario block and max-es it into norms[] when it leaves the
-    // block (integer max of |g| bit patterns: exact, order-independent).  No
-    // CTA barrier: warps cross block boundaries independently.
-    int32_t cur = -1;
-    // per-lane state that is touched once per item lives in shared memory,
-    // leaving the registers to the evaluation (B200, config 3: 0.598 -> 0.593 ms)
+    // current scenario block and max-es it into norms[] when it moves to a
+    // later block (a warp's blocks never go back, in either mode; integer
+    // max of |g| bit patterns: exact, order-independent).  No CTA barrier:
+    // warps cross block boundaries independently.  Per-lane state touched
+    // once per item lives in shared memory, leaving the registers to the
+    // evaluation (B200, config 3: 0.598 -> 0.593 ms).
     __shared__ unsigned long long s_nrm[W][32];
     __shared__ int32_t s_out[3][W][32];
+    __shared__ int32_t s_cur[W][32];
     unsigned long long& nrm = s_nrm[warp][lane];
     int32_t& out_l = s_out[0][warp][lane];
     int32_t& out_h = s_out[1][warp][lane];
     int32_t& out_k = s_out[2][warp][lane];
     nrm = 0;
     out_l = out_h = out_k = -1;   // lane's outaged branch and its buses
+    // the warp's current block: a register in static mode, shared memory in
+    // dynamic mode (whose claim bookkeeping needs the register)
+    int32_t cur_reg = -1;
+    int32_t& cur = DYN ? s_cur[warp][lane] : cur_reg;
+    cur = -1;
     auto flush = [&](int32_t blk) {
         if (MODE & NORM) {
             const int32_t s = blk * PF_LANES + lane;
@@ -775,40 +811,29 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         }
         nrm = 0;
     };
-    // prologue: item 0's copies in flight, item 1's record in a register
-    issue(blockIdx.x, rec_word(blockIdx.x), slots_u32);
-    int32_t rw_next = rec_word(blockIdx.x + stride);
-    int32_t k = 0;
-    for (int32_t item = blockIdx.x; item < n_items; item += stride, ++k) {
-        const int32_t blk = blk_of(item);
-        const int32_t grp = item - blk * n_groups;
-        if (blk != cur) {
-            if (cur >= 0) flush(cur);
-            cur = blk;
-            if (lane == 0) {
-                const int64_t b = blk;
-                A.y = y + b * d.n_var * PF_LANES;
-                A.g = g ? g + b * d.n_var * PF_LANES : nullptr;
-                A.j = jv ? jv + b * d.nnz * PF_LANES : nullptr;
-                A.pq_p = pq_p ? pq_p + b * d.P * PF_LANES : nullptr;
-                A.pq_q = pq_q ? pq_q + b * d.P * PF_LANES : nullptr;
-                A.pv_p = pv_p ? pv_p + b * d.G * PF_LANES : nullptr;
-            }
-            const int32_t s = blk * PF_LANES + lane;
-            out_l = (outage && s < K) ? __ldg(outage + s) : -1;
-            out_h = out_l >= 0 ? __ldg(d.bus_h + out_l) : -1;
-            out_k = out_l >= 0 ? __ldg(d.bus_k + out_l) : -1;
-            __syncwarp();
+    auto enter_block = [&](int32_t blk) {
+        if (cur >= 0) flush(cur);
+        cur = blk;
+        if (lane == 0) {
+            const int64_t b = blk;
+            A.y = y + b * d.n_var * PF_LANES;
+            A.g = g ? g + b * d.n_var * PF_LANES : nullptr;
+            A.j = jv ? jv + b * d.nnz * PF_LANES : nullptr;
+            A.pq_p = pq_p ? pq_p + b * d.P * PF_LANES : nullptr;
+            A.pq_q = pq_q ? pq_q + b * d.P * PF_LANES : nullptr;
+            A.pv_p = pv_p ? pv_p + b * d.G * PF_LANES : nullptr;
         }
-        unsigned char* sb = slots + (k & 1) * WS_SLOT_BYTES;
-        // next item's copies into the other slot (its previous contents,
-        // item k-1, were consumed in the previous iteration), then the
-        // record of the item after it
-        issue(item + stride, rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
-        rw_next = rec_word(item + 2 * stride);
-        cp_async_wait<1>();   // this item's group has landed (own lanes)
+        const int32_t s = blk * PF_LANES + lane;
+        out_l = (outage && s < K) ? __ldg(outage + s) : -1;
+        out_h = out_l >= 0 ? __ldg(d.bus_h + out_l) : -1;
+        out_k = out_l >= 0 ? __ldg(d.bus_k + out_l) : -1;
+        __syncwarp();
+    };
+    // evaluate step k (slot `slot` of block `blk`) from its staging slot
+    auto evaluate = [&](int32_t k, int32_t blk, int32_t slot) {
+        cp_async_wait<1>();   // this step's group has landed (own lanes)
         __syncwarp();         // ... and every lane's
-        const int32_t slot = grp * W + warp;
+        unsigned char* sb = slots + (k & 1) * WS_SLOT_BYTES;
         const int4* pk = reinterpret_cast<const int4*>(sb + WS_ROWS * WS_ROW_BYTES);
         const int4 cnt = pk[2];
         // does any lane's outaged branch end at this bus?  (usually not: then
@@ -823,6 +848,56 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
                                GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk));
         }
         __syncwarp();         // slot reads done before it is refilled
+    };
+
+    if constexpr (DYN) {
+        __shared__ int32_t s_q[W][4];      // claims of steps k .. k+2 (ring)
+        auto claim = [&]() -> int32_t {
+            int32_t q = 0;
+            if (lane == 0) q = atomicAdd(&s_ctr, 1);
+            return __shfl_sync(0xffffffffu, q, 0);
+        };
+        {   // prologue: step 0's copies in flight, step 1's record in a register
+            const int32_t q0 = claim();
+            issue(q0, rec_word(q0), slots_u32);
+            const int32_t q1 = claim();
+            if (lane == 0) {
+                s_q[warp][0] = q0;
+                s_q[warp][1] = q1;
+            }
+        }
+        __syncwarp();
+        int32_t rw_next = rec_word(s_q[warp][1]);
+        for (int32_t k = 0;; ++k) {
+            const int32_t q = s_q[warp][k & 3];
+            if (!live(q)) break;
+            const int32_t item = item_of(q);
+            const int32_t blk = blk_of(item);
+            if (blk != cur) enter_block(blk);
+            // claim step k+2; start step k+1's copies into the other slot
+            // (its previous contents, step k-1, were consumed in the previous
+            // iteration); load step k+2's record
+            const int32_t q2 = claim();
+            if (lane == 0) s_q[warp][(k + 2) & 3] = q2;
+            issue(s_q[warp][(k + 1) & 3], rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
+            rw_next = rec_word(q2);
+            evaluate(k, blk, (item - blk * n_groups) * W + q % W);
+        }
+    } else {
+        // prologue: item 0's copies in flight, item 1's record in a register
+        issue(blockIdx.x, rec_word(blockIdx.x), slots_u32);
+        int32_t rw_next = rec_word(blockIdx.x + stride);
+        int32_t k = 0;
+        for (int32_t item = blockIdx.x; item < n_items; item += stride, ++k) {
+            const int32_t blk = blk_of(item);
+            if (blk != cur) enter_block(blk);
+            // next item's copies into the other slot (its previous contents,
+            // item k-1, were consumed in the previous iteration), then the
+            // record of the item after it
+            issue(item + stride, rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
+            rw_next = rec_word(item + 2 * stride);
+            evaluate(k, blk, (item - blk * n_groups) * W + warp);
+        }
     }
     cp_async_wait<0>();
     if (cur >= 0) flush(cur);
@@ -1441,12 +1516,12 @@ static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const dou
 // Staged kernel shape (pf_internal.cuh WS_W, WS_MINB): two 4 KB slots per
 // warp in dynamic shared memory.
 constexpr size_t WS_SMEM = (size_t)WS_W * 2 * WS_SLOT_BYTES;
-template <int MODE>
-static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const double* y,
+template <int MODE, bool DYN>
+static cudaError_t launch_staged_kernel(const DevicePlan& d, int32_t K, const double* y,
                                       const double* pq_p, const double* pq_q,
                                       const double* pv_p, const int32_t* outage, double* g,
                                       double* j, double* norms, cudaStream_t st) {
-    auto kern = k_eval_staged<MODE, WS_W, WS_MINB>;
+    auto kern = k_eval_staged<MODE, WS_W, WS_MINB, DYN>;
     static int ctas = 0;
     static int sms = 0;
     if (!ctas) {
@@ -1473,6 +1548,19 @@ static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const doub
                                            reinterpret_cast<unsigned long long*>(norms), fd_m,
                                            fd_l);
     return cudaSuccess;
+}
+
+// Dynamic claiming when high-degree buses make the per-bus cost uneven
+// (>= 0.5 % of buses with degree >= HUB_DEG; B200, ms per launch, static /
+// dynamic: config 4 0.620 / 0.555, config 3 0.594 / 0.608).
+template <int MODE>
+static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const double* y,
+                                      const double* pq_p, const double* pq_q,
+                                      const double* pv_p, const int32_t* outage, double* g,
+                                      double* j, double* norms, cudaStream_t st) {
+    if ((int64_t)d.n_hubs * 200 >= d.N)
+        return launch_staged_kernel<MODE, true>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st);
+    return launch_staged_kernel<MODE, false>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st);
 }
 
 static bool use_staged() {

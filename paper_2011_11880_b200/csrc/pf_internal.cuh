@@ -100,7 +100,8 @@ struct DevicePlan {
                               // offsets of rows g_p[i], g_q[i], theta-block size,
                               // diagonal rank; [2i+1] = {e0, e1, t0, t1}: incidence
                               // and device-list ranges (one 32-byte load)
-    const int32_t* bus_order; // [N] batched processing order: degree >= HUB_DEG first
+    const int32_t* bus_order; // [N] batched processing order (hubs spread, then bus order)
+    int32_t n_hubs;           // buses with degree >= HUB_DEG
     const int4* ws_pkt;       // staged-kernel packets (see WS_ROWS above)
     const int4* ws_rec;       // [N * WS_REC_WORDS / 4] stage records in processing order
     const int32_t* dev_ptr;   // [N+1]

@@ -616,6 +616,7 @@ int build(const pf_topology* t, pf_plan** out) {
         std::stable_sort(hubs.begin(), hubs.end(), [&](int32_t a, int32_t b) {
             return hptr[a + 1] - hptr[a] > hptr[b + 1] - hptr[b];
         });
+        d.n_hubs = (int32_t)hubs.size();
         int dev = 0, sms = 0;
         PF_TRY(cudaGetDevice(&dev));
         PF_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
