@@ -188,3 +188,22 @@ def test_batched_lu_schedule_reference_solve_matches_scipy():
         x = BL.reference_factor_solve(sched, J.data, -g)
         ref = spla.spsolve(J.tocsc(), -g)
         assert np.abs(x - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("name", SINGLE + ["batch_edge300"])
+def test_q_limit_gen_rows_follow_build_system(name):
+    """newton._pv_gen_rows (the limit-switching loop's map from PV index to
+    gen row) follows build_system's PV numbering: same buses, setpoints and
+    scheduled powers, in order."""
+    from _util import case_of
+    from paper_2011_11880_b200.newton import _pv_gen_rows
+
+    raw = case_of(load(name))
+    s = build_system(raw)
+    rows = _pv_gen_rows(raw)
+    assert len(rows) == len(s.pv.bus)
+    order = np.argsort(raw.bus_id, kind="stable")
+    pos = order[np.searchsorted(raw.bus_id[order], raw.gen_bus[rows])]
+    assert np.array_equal(pos, s.pv.bus)
+    assert np.array_equal(raw.vg[rows], s.pv.v0)
+    assert np.array_equal(raw.pg[rows] / raw.base_mva, s.pv.p0)
