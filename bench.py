@@ -212,8 +212,14 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=dev)
 
     K = WORKLOADS[args.workload][1]
+    t0 = time.perf_counter()
     sys_ = build_case(args.workload)
+    t1 = time.perf_counter()
     plan = Plan(sys_, device=dev)
+    torch.cuda.synchronize(dev)
+    setup_s = {"build_system_s": t1 - t0, "plan_create_s": time.perf_counter() - t1,
+               "note": "synthetic case generation + build_system (host), then pf_plan_create: "
+                       "upload, device symbolic pattern, staging records"}
     per_scen, static, bytes_launch = algorithmic_bytes(sys_, plan.nnz, K)
     y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K, seed=1000 + rank)
     t = lambda a, dt=torch.float64: torch.from_numpy(a).to(dev, dt)
@@ -388,6 +394,7 @@ def run_gpu(args):
                                     if dr_err is None and dr_value > 0 else
                                     {"value": None, "error": dr_err or "failed on a peer rank"}),
             "gpu_launches": launches,
+            "setup": setup_s,
             "clocks": clk,
         }
     if world > 1:
