@@ -1558,7 +1558,13 @@ static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const doub
                                       const double* pq_p, const double* pq_q,
                                       const double* pv_p, const int32_t* outage, double* g,
                                       double* j, double* norms, cudaStream_t st) {
-    if ((int64_t)d.n_hubs * 200 >= d.N)
+    static int forced = -2;   // PF_SCHEDULE=static|dynamic overrides the choice (A/B, tests)
+    if (forced == -2) {
+        const char* e = getenv("PF_SCHEDULE");
+        forced = !e ? -1 : (e[0] == 'd' ? 1 : (e[0] == 's' ? 0 : -1));
+    }
+    const bool dyn = forced >= 0 ? forced == 1 : (int64_t)d.n_hubs * 200 >= d.N;
+    if (dyn)
         return launch_staged_kernel<MODE, true>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st);
     return launch_staged_kernel<MODE, false>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st);
 }

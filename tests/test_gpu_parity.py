@@ -833,8 +833,9 @@ def test_device_batched_sparse_lu_vs_scipy():
 
 def test_previous_batched_kernel_still_matches(tmp_path):
     """PF_BATCHED_KERNEL=old selects the previous single-role batched kernel
-    (kept for A/B timing, scripts/ab_env.sh); in a fresh process it must give
-    the same bits as the staged product kernel."""
+    (kept for A/B timing, scripts/ab_env.sh), PF_SCHEDULE forces the staged
+    kernel's static or dynamic schedule; in fresh processes every variant
+    must give the same bits as the default."""
     import subprocess
     import sys
 
@@ -860,16 +861,19 @@ np.savez(sys.argv[2], g=g.cpu().numpy(), j=j.cpu().numpy(), n=n.cpu().numpy())
 
     root = str(Path(__file__).resolve().parents[1])
     outs = {}
-    for kind in ("staged", "old"):
+    runs = {"staged": {}, "old": {"PF_BATCHED_KERNEL": "old"},
+            "static": {"PF_SCHEDULE": "static"}, "dynamic": {"PF_SCHEDULE": "dynamic"}}
+    for kind, extra in runs.items():
         env = dict(os.environ)
         env.pop("PF_BATCHED_KERNEL", None)
-        if kind == "old":
-            env["PF_BATCHED_KERNEL"] = "old"
+        env.pop("PF_SCHEDULE", None)
+        env.update(extra)
         f = tmp_path / f"{kind}.npz"
         subprocess.run([sys.executable, "-c", code, root, str(f)], check=True, env=env)
         outs[kind] = np.load(f)
-    for k in ("g", "j", "n"):
-        assert np.array_equal(outs["staged"][k], outs["old"][k]), k
+    for kind in ("old", "static", "dynamic"):
+        for k in ("g", "j", "n"):
+            assert np.array_equal(outs["staged"][k], outs[kind][k]), (kind, k)
 
 
 def test_newton_fallback_paths():
