@@ -109,6 +109,9 @@ WORKLOADS = {
 }
 
 
+SEED = 1000   # scenario seed of the bench workloads (tests/test_gpu_fullsize.py checks them)
+
+
 def build_case(workload: str = "config3"):
     from paper_2011_11880_b200 import synth
     from paper_2011_11880_b200.system_model import build_system
@@ -173,7 +176,7 @@ def run_reference(args):
     sys_ = build_case(args.workload)
     K = WORKLOADS[args.workload][1]
     threads = os.cpu_count() or 1
-    r = cpu_reference(sys_, K, 1000, args.steps, args.warmup, threads)
+    r = cpu_reference(sys_, K, SEED, args.steps, args.warmup, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "evals/s",
         "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
@@ -221,7 +224,7 @@ def run_gpu(args):
                "note": "synthetic case generation + build_system (host), then pf_plan_create: "
                        "upload, device symbolic pattern, staging records"}
     per_scen, static, bytes_launch = algorithmic_bytes(sys_, plan.nnz, K)
-    y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K, seed=1000 + rank)
+    y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K, seed=SEED + rank)
     t = lambda a, dt=torch.float64: torch.from_numpy(a).to(dev, dt)
     d_y, d_pqp, d_pqq, d_pvp = t(y), t(pq_p), t(pq_q), t(pv_p)
     d_out = torch.from_numpy(outage).to(dev)

@@ -3,9 +3,8 @@
 // Compiled with -fmad=false: every product and sum is rounded exactly where
 // the reference's wf1 rounds it (numba njit without fastmath, pflow
 // kernels.py:79-282), so the only deviation from the CPU oracle is the last
-// rounding of sin/cos: pf_trig.h is correctly rounded except in rare
-// near-midpoint cases, and glibc 2.39 is not correctly rounded in ~0.3% of
-// power-flow angles, so the two agree on >99.7% of arguments.
+// rounding of sin/cos -- and pf_trig.h restates glibc 2.39's sin/cos bit for
+// bit (checked against the live libm on 2e9 arguments), so there is none.
 //
 // Fused kernel k_eval (the product path): one thread per (bus, scenario).
 // A bus walks its incidence list -- branches with h = bus ascending, then
@@ -33,8 +32,8 @@ namespace {
 constexpr int RES = 1, JAC = 2, NORM = 4;
 
 // The one trig routine every kernel uses (fused, per-model, test surface):
-// near-correctly-rounded table sin/cos (pf_trig.h), table staged in shared
-// memory because lanes index it divergently.
+// glibc-identical table sin/cos (pf_trig.h), table staged in shared memory
+// because lanes index it divergently.
 __device__ __forceinline__ void pf_sincos(double x, const double* tab, double* s, double* c) {
     pf_sincos_tab(x, tab, s, c);
 }
@@ -1083,18 +1082,24 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
     // barrier (it is not read before).
     const int4 c0 = __ldg(d.sg_chunk + 2 * blockIdx.x);
     const int4 c1 = __ldg(d.sg_chunk + 2 * blockIdx.x + 1);
-    constexpr int TAB = PF_TRIG_N * 4;
-    static_assert(TAB <= 2 * SG_THREADS, "trig table staging");
-    const double tv0 = __ldg(pf_trig_tab + t);
-    const double tv1 = t + SG_THREADS < TAB ? __ldg(pf_trig_tab + t + SG_THREADS) : 0.0;
+    // trig table: 16-byte cp.async copies straight into shared memory (no
+    // registers held across the plan loads); waited for at the first barrier
+    constexpr int TAB16 = PF_TRIG_N * 4 / 2;
+    static_assert(TAB16 <= 2 * SG_THREADS, "trig table staging");
+    {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_tab);
+        for (int c = t; c < TAB16; c += SG_THREADS)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * c),
+                         "l"(pf_trig_tab + 2 * c) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     const double* tab = s_tab;
     const int32_t b0 = c0.x, b1 = c0.y & ~SG_BIG, E0 = c0.z, E1 = c0.w;
     const Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
     unsigned long long nrm = 0;
     if (c0.y & SG_BIG) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        s_tab[t] = tv0;
-        if (t + SG_THREADS < TAB) s_tab[t + SG_THREADS] = tv1;
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         if (t == 0) nrm = eval_bus<MODE, 1>(d, tab, b0, A, 0, -1);
     } else {
@@ -1135,8 +1140,6 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             single_dev_plan(src, d, t0, nd > 0, src.dv0, src.a0, src.b0, src.c0, src.d0);
             single_dev_plan(src, d, t0 + 1, nd > 1, src.dv1, src.a1, src.b1, src.c1, src.d1);
         }
-        s_tab[t] = tv0;
-        if (t + SG_THREADS < TAB) s_tab[t + SG_THREADS] = tv1;
         // state: after the preceding kernel's writes are visible
         asm volatile("griddepcontrol.wait;" ::: "memory");
         double tja = 0.0, wja = 0.0, tjb = 0.0, wjb = 0.0;
@@ -1157,6 +1160,7 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             bv[t] = src.vi;
             bnb[t] = src.h0.z;
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         auto incidence = [&](int32_t e, int4 r, double4 c, double tj, double wj) {   // phase A
             const int32_t o = r.y & SG_FIELD_MASK;

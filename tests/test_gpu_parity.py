@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 
 import oracle
-from _util import (SINGLE, assert_parity, csc_to_csr_perm, load, parity_failures, system_of)
+from _util import (SINGLE, assert_parity, bit_mismatches, csc_to_csr_perm, load, parity_failures,
+                   system_of)
 from paper_2011_11880_b200 import synth
 from paper_2011_11880_b200.system_model import build_system, random_state
 
@@ -301,6 +302,7 @@ def test_stress_hubs_config4_shape():
     fails = sum(parity_failures(G[k], g_ref[k]) + parity_failures(J[k][perm], j_ref[k])
                 for k in range(K))
     assert fails == 0
+    assert bit_mismatches(G, g_ref) == 0 and bit_mismatches(J[:, perm], j_ref) == 0
     # the single-grid kernel on the same hub topology (chunks hold the hubs)
     y = random_state(s, 77)
     g, j, norm = _eval(plan, y)
@@ -357,19 +359,25 @@ def test_deterministic_repeat():
     assert all(np.array_equal(x, y_) for x, y_ in zip(plan.pattern_csr(), plan2.pattern_csr()))
 
 
-def test_gpu_trig_bit_identical_to_cpu_twin(tmp_path):
+def test_gpu_trig_bit_identical_to_glibc(tmp_path):
+    """The device sin/cos (csrc/pf_trig.h) against this host's libm sin()
+    and cos() -- what pflow wf1 calls -- and against the CPU twin, bit for
+    bit, over every range the restatement covers (|x| < 105414350)."""
     from test_trig import build_twin, sample, twin_sincos
 
     from paper_2011_11880_b200.plan import sincos
 
-    x = sample(200000, seed=5)
-    s_ref, c_ref = twin_sincos(build_twin(tmp_path), x)
+    x = sample(2_000_000, seed=5)
     s, c = sincos(torch.as_tensor(x, device="cuda"))
     s, c = s.cpu().numpy(), c.cpu().numpy()
-    finite = np.abs(x) < 2.0 ** 20
-    assert np.array_equal(s[finite], s_ref[finite])
-    assert np.array_equal(c[finite], c_ref[finite])
-    assert np.array_equal(np.signbit(s[finite]), np.signbit(s_ref[finite]))
+    s_ref, c_ref = twin_sincos(build_twin(tmp_path), x)
+    g_s, g_c = oracle.libm_sincos(x)
+    cover = ~(np.abs(x) >= float.fromhex("0x1.921fbp+26"))      # NaN included
+    for got, ref in ((s, g_s), (c, g_c), (s, s_ref), (c, c_ref)):
+        assert np.array_equal(got[cover].view(np.int64), ref[cover].view(np.int64))
+    # beyond: still odd / even and close (the library reduction is not restated)
+    big = ~cover & np.isfinite(x)
+    assert np.abs(s[big] - g_s[big]).max(initial=0) < 1e-15
 
 
 @pytest.mark.parametrize("name", ["case2", "case5_shift", "case14", "slack_only"])
@@ -423,7 +431,11 @@ def test_config4_full_size_sampled_scenarios():
         assert_parity(J[k][perm], j_ref[i], f"config4 scenario {k} J")
 
 
-@pytest.mark.parametrize("seed", range(12))
+# 100 seeded grids, plus seed 903: the one grid of round 1's 1,430-grid
+# campaign whose batched residual missed the 1e-12 bound (1.27e-12 on a
+# heavily cancelling bus, from a one-ulp sin/cos difference with glibc) --
+# now bit-identical.
+@pytest.mark.parametrize("seed", [*range(100), 903])
 def test_random_grids_fuzz(seed):
     """Randomised small grids (parallel and reversed branches, shifts, taps,
     shunts, out-of-service rows, hubs, isolated buses): pattern bit-exact and

@@ -125,6 +125,12 @@ def test_sincos_poly_accuracy():
 
 
 def test_assert_parity_helper():
-    assert_parity(np.array([1.0, 0.0]), np.array([1.0 + 1e-13, 5e-15]))
+    assert_parity(np.array([1.0, 0.0]), np.array([1.0 + 1e-13, 5e-15]), bitwise=False)
     with pytest.raises(AssertionError):
-        assert_parity(np.array([1.0]), np.array([1.0 + 1e-11]))
+        assert_parity(np.array([1.0]), np.array([1.0 + 1e-11]), bitwise=False)
+    # the default also demands bit-identity (signed zeros included)
+    assert_parity(np.array([1.0, -0.0]), np.array([1.0, -0.0]))
+    with pytest.raises(AssertionError, match="bit-identical"):
+        assert_parity(np.array([1.0]), np.array([1.0 + 1e-13]))
+    with pytest.raises(AssertionError, match="bit-identical"):
+        assert_parity(np.array([0.0]), np.array([-0.0]))
