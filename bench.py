@@ -101,15 +101,23 @@ class Clocks:
 
 
 WORKLOADS = {
-    # name: (BASELINE config, scenarios per GPU, description)
-    "config3": (3, 256, "config3: 70k-bus/88k-branch grid (45k PQ, 6k PV, 1 slack), "
-                        "K=256 scenarios per GPU per step"),
-    "config4": (4, 64, "config4 stress: 200k-bus/250k-branch grid + 1% degree-50 hub buses, "
-                       "K=64 scenarios per GPU per step"),
+    # name: (BASELINE config, scenarios, default scaling, description)
+    # config 3 is "K=256 sharded across 1/2/4/8 B200" (strong: the same 256
+    # scenarios split over the ranks); config 4 is "K=64 scenarios per GPU"
+    # (weak: every rank evaluates its own 64).
+    "config3": (3, 256, "strong", "config3: 70k-bus/88k-branch grid (45k PQ, 6k PV, 1 slack), "
+                                  "K=256 scenarios per step"),
+    "config4": (4, 64, "weak", "config4 stress: 200k-bus/250k-branch grid + 1% degree-50 hub "
+                               "buses, K=64 scenarios per GPU per step"),
 }
-
-
 SEED = 1000   # scenario seed of the bench workloads (tests/test_gpu_fullsize.py checks them)
+SCEN = ("per-device load U(0.8,1.2) + PV U(0.5,1.5) scaling, 1 outaged branch each; "
+        "fused f+J+inf-norm")
+
+
+def workload_desc(workload: str) -> str:
+    """The workload string both arms print (so the driver sees one config)."""
+    return f"{WORKLOADS[workload][3]}, {SCEN}"
 
 
 def build_case(workload: str = "config3"):
@@ -120,13 +128,30 @@ def build_case(workload: str = "config3"):
     return build_system(synth.config_case(cfg, seed=cfg))
 
 
-def blocked_inputs(sys_, K, seed):
+def blocked_inputs(sys_, K, seed, lo: int = 0, hi: int | None = None):
+    """Blocked-layout inputs of scenarios [lo, hi) of the K-scenario batch
+    drawn with ``seed`` (a rank's shard; the whole batch by default)."""
     from paper_2011_11880_b200 import synth
     from paper_2011_11880_b200.plan import to_blocked
 
+    hi = K if hi is None else hi
     sb = synth.make_scenarios(sys_, K, seed)
-    return (to_blocked(sb.y.T), to_blocked(sb.pq_p.T), to_blocked(sb.pq_q.T),
-            to_blocked(sb.pv_p.T), sb.outage.astype(np.int32))
+    c = lambda a: np.ascontiguousarray(a[:, lo:hi].T)
+    return (to_blocked(c(sb.y)), to_blocked(c(sb.pq_p)), to_blocked(c(sb.pq_q)),
+            to_blocked(c(sb.pv_p)), np.ascontiguousarray(sb.outage[lo:hi], dtype=np.int32))
+
+
+def rank_workload(workload: str, scaling: str, rank: int, world: int):
+    """(K_total, lo, hi, seed, K_gen) of this rank: strong scaling splits the
+    workload's K scenarios with batched.shard; weak scaling gives every rank
+    its own K (seed SEED + rank)."""
+    from paper_2011_11880_b200.batched import shard
+
+    K = WORKLOADS[workload][1]
+    if scaling == "strong":
+        lo, hi = shard(K, rank, world)
+        return K, lo, hi, SEED, K
+    return K * world, 0, K, SEED + rank, K
 
 
 # ---------------------------------------------------------------------------
@@ -177,14 +202,15 @@ def run_reference(args):
     K = WORKLOADS[args.workload][1]
     threads = os.cpu_count() or 1
     r = cpu_reference(sys_, K, SEED, args.steps, args.warmup, threads)
+    scaling = args.scaling or WORKLOADS[args.workload][2]
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "evals/s",
         "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
-        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][2] + " (load/PV scaling + 1 outage "
-                               "each), f+J per scenario",
-                   "parallelism": f"{threads} host threads, one scenario per thread at a time"},
+        "config": {"workload": workload_desc(args.workload),
+                   "parallelism": f"{threads} host threads, one scenario per thread at a time "
+                                  "(CPU only; the N GPUs are unused)"},
         "cpu_baseline": {"value": r["value"], "unit": "evals/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{r['steps']} steps x {K} scenarios, pflow wf{r['wf']} "
@@ -200,23 +226,33 @@ def run_reference(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 
-def run_gpu(args):
+def traffic_of(workload: str):
+    """ncu DRAM bytes per launch of the product kernel, only when
+    profiles/traffic.json was captured from this very kernel source."""
+    from paper_2011_11880_b200.build import source_hash
+
+    tfile = ROOT / "profiles" / "traffic.json"
+    if not tfile.exists():
+        return None
+    ent = json.loads(tfile.read_text()).get(workload, {})
+    return ent.get("bytes") if ent.get("source_hash") == source_hash() else None
+
+
+def batched_leg(args, workload: str, scaling: str, dev, rank: int, world: int,
+                e2e: bool) -> dict | None:
+    """One scenario-batched workload on this rank's shard.  Returns rank 0's
+    result dict (None elsewhere).  Every rank joins every collective."""
     import torch
     import torch.distributed as dist
 
+    from paper_2011_11880_b200.batched import NormExchange, max_shard
     from paper_2011_11880_b200.plan import Plan, launch_count
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    K = WORKLOADS[args.workload][1]
+    K_total, lo, hi, seed, K_gen = rank_workload(workload, scaling, rank, world)
+    K = hi - lo
+    kmax = max_shard(K_gen, world) if scaling == "strong" else K
     t0 = time.perf_counter()
-    sys_ = build_case(args.workload)
+    sys_ = build_case(workload)
     t1 = time.perf_counter()
     plan = Plan(sys_, device=dev)
     torch.cuda.synchronize(dev)
@@ -224,26 +260,32 @@ def run_gpu(args):
                "note": "synthetic case generation + build_system (host), then pf_plan_create: "
                        "upload, device symbolic pattern, staging records"}
     per_scen, static, bytes_launch = algorithmic_bytes(sys_, plan.nnz, K)
-    y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K, seed=SEED + rank)
+    y, pq_p, pq_q, pv_p, outage = blocked_inputs(sys_, K_gen, seed, lo, hi)
     t = lambda a, dt=torch.float64: torch.from_numpy(a).to(dev, dt)
     d_y, d_pqp, d_pqq, d_pvp = t(y), t(pq_p), t(pq_q), t(pv_p)
     d_out = torch.from_numpy(outage).to(dev)
     d_g = plan.empty(plan.n_var, K)
     d_j = plan.empty(plan.nnz, K)
-    d_n = plan.empty(K)
+    # double-buffered norms: the all-gather of step i (NCCL, on its own
+    # stream) overlaps step i+1's evaluation (batched.NormExchange)
+    nx = NormExchange(kmax, dev)
     stream = torch.cuda.current_stream(dev)
-    gathered = torch.empty(world * K, dtype=torch.float64, device=dev)
 
-    def step():
-        plan.eval_batched(K, d_y, d_pqp, d_pqq, d_pvp, d_out, d_g, d_j, d_n, stream=stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, d_n)
+    def step(i, ev=None):
+        nrm = nx.buffer(i)            # waits (stream-side) for gather i-2
+        if ev is not None:
+            ev[0].record(stream)
+        plan.eval_batched(K, d_y, d_pqp, d_pqq, d_pvp, d_out, d_g, d_j, nrm, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        nx.start(i)
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
+    nx.drain()
     torch.cuda.synchronize(dev)
 
-    clocks = Clocks(local)
+    clocks = Clocks(dev.index)
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -254,11 +296,8 @@ def run_gpu(args):
     l0 = launch_count()
     start.record(stream)
     for i in range(args.steps):
-        ev[i][0].record(stream)
-        plan.eval_batched(K, d_y, d_pqp, d_pqq, d_pvp, d_out, d_g, d_j, d_n, stream=stream)
-        ev[i][1].record(stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, d_n)
+        step(i, ev[i])
+    nx.drain()                        # the last norms are gathered inside the timed region
     end.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -270,17 +309,35 @@ def run_gpu(args):
     ms_t = torch.tensor([ms_total, statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_total, kern_avg = float(ms_t[0]), float(ms_t[1])
-    value = world * K * args.steps / (ms_total / 1e3)
+    ms_total, kern_max = float(ms_t[0]), float(ms_t[1])
+    kern_avg = statistics.mean(kern_ms)
+    value = K_total * args.steps / (ms_total / 1e3)
     peak, peak_kind = peaks()
     achieved = bytes_launch / (kern_avg / 1e3) / 1e9
-    traffic = None
-    tfile = ROOT / "profiles" / "traffic.json"
-    if tfile.exists():  # measured by ncu on this kernel (see that file's note)
-        traffic = json.loads(tfile.read_text()).get(args.workload, {}).get("bytes")
+    last = args.steps - 1
+    assert torch.isfinite(nx.local[last & 1][:K]).all()
+    assert torch.equal(nx.result(last)[rank, :K], nx.local[last & 1][:K])   # arrived intact
 
-    # norms sanity (device-resident result used by Newton callers)
-    assert torch.isfinite(d_n[:K]).all()
+    out = None
+    if rank == 0:
+        out = {
+            "value": value, "ms_per_step": ms_total / args.steps, "scaling": scaling,
+            "workload": workload_desc(workload), "scenarios_total": K_total,
+            "scenarios_per_gpu": K, "gpu_launches": launches, "clocks": clk,
+            "n_var": plan.n_var, "nnz": plan.nnz, "max_bus_degree": plan.max_degree,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic_of(workload),
+                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_launch,
+                         "bytes_per_scenario": per_scen, "static_bytes": static,
+                         "kernel_ms": kern_avg, "kernel_ms_max_over_ranks": kern_max,
+                         "kernel": "k_eval_staged<RES|JAC|NORM>"},
+            "l2": f"inputs+outputs per launch {bytes_launch / 1e9:.2f} GB > 126 MB L2 "
+                  "(no flush needed)" if bytes_launch > 126e6 else
+                  f"inputs+outputs per launch {bytes_launch / 1e6:.0f} MB",
+            "setup": setup_s,
+        }
+    if not e2e:
+        return out
 
     # ---- e2e through the host-buffer C ABI (pinned host memory) ----
     # (an error here is reported in the line; every rank still joins the
@@ -318,29 +375,28 @@ def run_gpu(args):
     e2e_s = torch.tensor([elapsed], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = world * K * e2e_steps / float(e2e_s[0])
+    e2e_value = K_total * e2e_steps / float(e2e_s[0])
 
     # ---- e2e, device-resident workflow (the north star's: g and J stay on
     # the GPU for a device solver; only the per-scenario norms come back) ----
     dr_err = None
-    dr_value = None
     try:
         pt = lambda a: torch.from_numpy(a).pin_memory()
         hp = [pt(a) for a in (y, pq_p, pq_q, pv_p)]
         hp_out = pt(outage)
         dp = [torch.empty_like(a, device=dev) for a in hp]
         dp_out = torch.empty_like(hp_out, device=dev)
-        hn = torch.empty(K, dtype=torch.float64).pin_memory()
+        hn = torch.empty(world * kmax, dtype=torch.float64).pin_memory()
 
         def dr_step():
             for a, b in zip(dp, hp):
                 a.copy_(b, non_blocking=True)
             dp_out.copy_(hp_out, non_blocking=True)
-            plan.eval_batched(K, dp[0], dp[1], dp[2], dp[3], dp_out, d_g, d_j, d_n,
+            nrm = nx.buffer(0)
+            plan.eval_batched(K, dp[0], dp[1], dp[2], dp[3], dp_out, d_g, d_j, nrm,
                               stream=stream)
-            if world > 1:
-                dist.all_gather_into_tensor(gathered, d_n)
-            hn.copy_(d_n[:K], non_blocking=True)
+            nx.start(0)
+            hn.copy_(nx.result(0).reshape(-1), non_blocking=True)
             torch.cuda.synchronize(dev)
 
         dr_step()
@@ -359,51 +415,80 @@ def run_gpu(args):
     dr_s = torch.tensor([elapsed], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(dr_s, op=dist.ReduceOp.MAX)
-    dr_value = world * K * e2e_steps / float(dr_s[0])
+    dr_value = K_total * e2e_steps / float(dr_s[0])
+    if rank == 0:
+        out["e2e"] = ({"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": bi,
+                       "d2h_bytes_per_step": bo,
+                       "api": "pf_eval_batched_host (pinned host buffers)", "steps": e2e_steps}
+                      if e2e_err is None and e2e_value > 0 else
+                      {"value": None, "unit": "evals/s",
+                       "error": e2e_err or "failed on a peer rank"})
+        out["e2e_device_resident"] = (
+            {"value": dr_value, "unit": "evals/s", "h2d_bytes_per_step": bi,
+             "d2h_bytes_per_step": 8 * world * kmax,
+             "api": "pinned inputs -> device, pf_eval_batched, norms -> host; g and J stay "
+                    "in HBM for a device solver", "steps": e2e_steps}
+            if dr_err is None and dr_value > 0 else
+            {"value": None, "error": dr_err or "failed on a peer rank"})
+    return out
 
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    scaling = args.scaling or WORKLOADS[args.workload][2]
+    head = batched_leg(args, args.workload, scaling, dev, rank, world, e2e=True)
     line = None
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "metric": METRIC, "value": head["value"], "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {
-                "workload": WORKLOADS[args.workload][2] + ", per-device load U(0.8,1.2) + "
-                            "PV U(0.5,1.5) scaling, 1 outaged branch each; fused f+J+inf-norm",
-                "n_var": plan.n_var, "nnz": plan.nnz, "scenarios_per_gpu": K,
-                "parallelism": f"scenario-sharded x{world}" + (", NCCL all-gather of norms"
-                                                               if world > 1 else ""),
-                "l2": f"inputs+outputs per step {bytes_launch / 1e9:.2f} GB > 126 MB L2 "
-                      "(no flush needed)",
-                "max_bus_degree": plan.max_degree,
+                "workload": head["workload"], "n_var": head["n_var"], "nnz": head["nnz"],
+                "scenarios_total": head["scenarios_total"],
+                "scenarios_per_gpu": head["scenarios_per_gpu"],
+                "parallelism": f"scenario-sharded x{world} ({scaling} scaling)"
+                               + (", NCCL all-gather of norms overlapped with the next step"
+                                  if world > 1 else ""),
+                "l2": head["l2"], "max_bus_degree": head["max_bus_degree"],
             },
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": bytes_launch,
-                         "bytes_per_scenario": per_scen, "static_bytes": static,
-                         "kernel_ms": kern_avg, "kernel": "k_eval_staged<RES|JAC|NORM>"},
-            "e2e": ({"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": bi,
-                     "d2h_bytes_per_step": bo,
-                     "api": "pf_eval_batched_host (pinned host buffers)", "steps": e2e_steps}
-                    if e2e_err is None and e2e_value > 0 else
-                    {"value": None, "unit": "evals/s", "error": e2e_err or "failed on a peer rank"}),
-            "e2e_device_resident": ({"value": dr_value, "unit": "evals/s",
-                                     "h2d_bytes_per_step": bi, "d2h_bytes_per_step": 8 * K,
-                                     "api": "pinned inputs -> device, pf_eval_batched, norms "
-                                            "-> host; g and J stay in HBM for a device solver",
-                                     "steps": e2e_steps}
-                                    if dr_err is None and dr_value > 0 else
-                                    {"value": None, "error": dr_err or "failed on a peer rank"}),
-            "gpu_launches": launches,
-            "setup": setup_s,
-            "clocks": clk,
+            "roofline": head["roofline"], "e2e": head["e2e"],
+            "e2e_device_resident": head["e2e_device_resident"],
+            "gpu_launches": head["gpu_launches"], "setup": head["setup"],
+            "clocks": head["clocks"],
         }
-    if world > 1:
-        dist.barrier()
 
     # optional legs: a failure there is reported in the line, never loses it
+    if args.workload == "config3" and not args.no_config4:
+        try:
+            c4 = batched_leg(args, "config4", WORKLOADS["config4"][2], dev, rank, world,
+                             e2e=False)
+        except Exception as e:  # noqa: BLE001
+            c4 = {"error": repr(e)}
+        if rank == 0:
+            line["config4"] = c4
+            if world == 1 and not args.no_cpu and "error" not in c4:
+                try:
+                    threads = os.cpu_count() or 1
+                    s4 = build_case("config4")
+                    r = cpu_reference(s4, 64, SEED, 1, 1, threads, min_seconds=args.cpu_seconds)
+                    c4["cpu_baseline"] = {
+                        "value": r["value"], "unit": "evals/s", "cores": threads, "kind": "port",
+                        "sample": f"{r['steps']} x 64 config4 scenarios, pflow wf{r['wf']} "
+                                  "restated in C (oracle/), one scenario per thread"}
+                except Exception as e:  # noqa: BLE001
+                    c4["cpu_baseline"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_single and args.workload == "config3":
         try:
             line["single_grid"] = single_grid(dev, steps=max(20, args.steps),
@@ -413,7 +498,9 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         try:
-            r = cpu_reference(sys_, K, 2000, 1, 1, threads, min_seconds=args.cpu_seconds)
+            sys_ = build_case(args.workload)
+            K = WORKLOADS[args.workload][1]
+            r = cpu_reference(sys_, K, SEED, 1, 1, threads, min_seconds=args.cpu_seconds)
             line["cpu_baseline"] = {
                 "value": r["value"], "unit": "evals/s", "cores": threads, "kind": "port",
                 "sample": f"{r['steps']} x {K} {args.workload} scenarios, pflow wf{r['wf']} "
@@ -423,6 +510,7 @@ def run_gpu(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 
@@ -590,6 +678,10 @@ def main():
     ap.add_argument("--no-single", action="store_true", help="skip the single-grid leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="strong: split the workload's K over the ranks (config 3 default); "
+                         "weak: K per rank (config 4 default)")
+    ap.add_argument("--no-config4", action="store_true", help="skip the config-4 leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -120,7 +120,8 @@ PF_API int pf_eval(const pf_plan* plan, const double* y, double* g, double* jval
 /* K scenarios over the shared topology (device pointers, batched layout).
  * y: n_var entries; pq_p/pq_q: n_pq entries; pv_p: n_pv entries (NULL = the
  * plan's base values); outage[K]: branch index zeroed in that scenario, -1 =
- * none (NULL = no outages).  Outputs g (n_var entries), jval (nnz entries,
+ * none (NULL = no outages; an index outside [-1, n_line) is treated as none
+ * here and rejected with PF_EINVAL by pf_eval_batched_host).  Outputs g (n_var entries), jval (nnz entries,
  * CSR order), norms[K] = max_r |g_s[r]|; any may be NULL.  Equivalent to
  * mutating pflow.PowerSystem arrays per scenario and running wf1. */
 PF_API int pf_eval_batched(const pf_plan* plan, int32_t K, const double* y, const double* pq_p,

@@ -29,6 +29,20 @@ UNITS = {
 }
 
 
+def source_hash() -> str:
+    """Hash of every kernel source and the compile flags: identifies the build
+    an ncu capture was taken from (profiles/traffic.json)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for p in sorted([*CSRC.glob("*.cu"), *CSRC.glob("*.h"), *CSRC.glob("*.cuh"),
+                     ROOT / "include" / "pfgpu.h"]):
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    h.update(repr((COMMON, UNITS)).encode())
+    return h.hexdigest()[:16]
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (Path(cand).exists() or cand == "nvcc"):

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "pf_internal.cuh"
 #include "pf_trig.h"
@@ -537,6 +538,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_batched(
             }
             const int32_t s = blk * PF_LANES + lane;
             out_l = (outage && s < K) ? __ldg(outage + s) : -1;
+            if ((uint32_t)out_l >= (uint32_t)d.L) out_l = -1;   // out of range: no outage
             __syncthreads();
         }
         // processing order: high-degree buses first, so they do not form a
@@ -824,6 +826,8 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         }
         const int32_t s = blk * PF_LANES + lane;
         out_l = (outage && s < K) ? __ldg(outage + s) : -1;
+        // an index outside [0, L) (rejected by the host paths) reads no memory
+        if ((uint32_t)out_l >= (uint32_t)d.L) out_l = -1;
         out_h = out_l >= 0 ? __ldg(d.bus_h + out_l) : -1;
         out_k = out_l >= 0 ? __ldg(d.bus_k + out_l) : -1;
         __syncwarp();
@@ -1435,15 +1439,48 @@ inline unsigned grid_for(int64_t n, int threads) {
 
 // ---- launchers --------------------------------------------------------------
 
+// Per-device launch configuration of one kernel instantiation: the
+// dynamic-shared-memory opt-in (a per-context function attribute), the SM
+// count and the occupancy, set up once per device ordinal (std::call_once:
+// concurrent first launches from several host threads are safe), with the
+// CUDA status kept and returned on every launch.
+constexpr int PF_MAX_DEVICES = 64;
+struct DevLaunchCfg {
+    std::once_flag once;
+    cudaError_t err = cudaSuccess;
+    int ctas = 1;
+    int sms = 1;
+};
+
+template <class Kern>
+static cudaError_t device_cfg(DevLaunchCfg (&tab)[PF_MAX_DEVICES], Kern kern, int threads,
+                              size_t dyn_smem, const DevLaunchCfg** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= PF_MAX_DEVICES) return cudaErrorInvalidDevice;
+    DevLaunchCfg& c = tab[dev];
+    std::call_once(c.once, [&] {
+        c.err = cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (c.err == cudaSuccess && dyn_smem > 48 * 1024)
+            c.err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dyn_smem);
+        if (c.err == cudaSuccess)
+            c.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.ctas, kern, threads,
+                                                                  dyn_smem);
+        if (c.ctas < 1) c.ctas = 1;
+    });
+    *out = &c;
+    return c.err;
+}
+
 template <int MODE>
 static cudaError_t launch_single_mode(const DevicePlan& d, const double* y, double* g, double* j,
                                       double* norm, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_eval_single<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)SG_SMEM_BYTES);
-        configured = true;
-    }
+    static DevLaunchCfg tab[PF_MAX_DEVICES];
+    const DevLaunchCfg* dc = nullptr;
+    cudaError_t e = device_cfg(tab, k_eval_single<MODE>, SG_THREADS, SG_SMEM_BYTES, &dc);
+    if (e != cudaSuccess) return e;
     // programmatic stream serialisation: see k_eval_single
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(d.sg_chunks);
@@ -1495,16 +1532,12 @@ static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const dou
                                        const double* pq_p, const double* pq_q,
                                        const double* pv_p, const int32_t* outage, double* g,
                                        double* j, double* norms, cudaStream_t st) {
-    static int ctas = 0;  // resident CTAs per SM for this instantiation
-    static int sms = 0;
-    if (!ctas) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &ctas, k_eval_batched<MODE, BATCH_W, BATCH_MINB>, 32 * BATCH_W, 0);
-        if (ctas < 1) ctas = 1;
-    }
+    static DevLaunchCfg tab[PF_MAX_DEVICES];
+    const DevLaunchCfg* dc = nullptr;
+    cudaError_t e = device_cfg(tab, k_eval_batched<MODE, BATCH_W, BATCH_MINB>, 32 * BATCH_W, 0,
+                               &dc);
+    if (e != cudaSuccess) return e;
+    const int ctas = dc->ctas, sms = dc->sms;
     const int32_t n_groups = (d.N + BATCH_W - 1) / BATCH_W;
     const int64_t n_items64 = (int64_t)n_groups * ((K + PF_LANES - 1) / PF_LANES);
     if (n_items64 >= (1ll << 31)) return cudaErrorInvalidValue;
@@ -1526,16 +1559,11 @@ static cudaError_t launch_staged_kernel(const DevicePlan& d, int32_t K, const do
                                       const double* pv_p, const int32_t* outage, double* g,
                                       double* j, double* norms, cudaStream_t st) {
     auto kern = k_eval_staged<MODE, WS_W, WS_MINB, DYN>;
-    static int ctas = 0;
-    static int sms = 0;
-    if (!ctas) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, 32 * WS_W, WS_SMEM);
-        if (ctas < 1) ctas = 1;
-    }
+    static DevLaunchCfg tab[PF_MAX_DEVICES];
+    const DevLaunchCfg* dc = nullptr;
+    cudaError_t e = device_cfg(tab, kern, 32 * WS_W, WS_SMEM, &dc);
+    if (e != cudaSuccess) return e;
+    const int ctas = dc->ctas, sms = dc->sms;
     const int32_t n_groups = (d.N + WS_W - 1) / WS_W;
     const int64_t n_items64 = (int64_t)n_groups * ((K + PF_LANES - 1) / PF_LANES);
     if (n_items64 >= (1ll << 31)) return cudaErrorInvalidValue;
@@ -1562,11 +1590,12 @@ static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const doub
                                       const double* pq_p, const double* pq_q,
                                       const double* pv_p, const int32_t* outage, double* g,
                                       double* j, double* norms, cudaStream_t st) {
-    static int forced = -2;   // PF_SCHEDULE=static|dynamic overrides the choice (A/B, tests)
-    if (forced == -2) {
+    // PF_SCHEDULE=static|dynamic overrides the choice (A/B, tests); read once
+    // (a C++11 function-local static initialiser is thread-safe)
+    static const int forced = [] {
         const char* e = getenv("PF_SCHEDULE");
-        forced = !e ? -1 : (e[0] == 'd' ? 1 : (e[0] == 's' ? 0 : -1));
-    }
+        return !e ? -1 : (e[0] == 'd' ? 1 : (e[0] == 's' ? 0 : -1));
+    }();
     const bool dyn = forced >= 0 ? forced == 1 : (int64_t)d.n_hubs * 200 >= d.N;
     if (dyn)
         return launch_staged_kernel<MODE, true>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st);
@@ -1574,12 +1603,11 @@ static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const doub
 }
 
 static bool use_staged() {
-    static int v = -1;
-    if (v < 0) {
+    static const bool v = [] {
         const char* e = getenv("PF_BATCHED_KERNEL");
-        v = !(e && e[0] == 'o');   // "old": the single-role kernel (A/B timing)
-    }
-    return v == 1;
+        return !(e && e[0] == 'o');   // "old": the single-role kernel (A/B timing)
+    }();
+    return v;
 }
 
 cudaError_t launch_eval_batched(const DevicePlan& d, int32_t K, const double* y,

@@ -979,6 +979,10 @@ int pf_eval_batched_host(pf_plan* p, int32_t K, const double* y, const double* p
                          int32_t n_streams) {
     if (!p || !y) return pf::invalid("NULL argument");
     if (K <= 0) return PF_OK;
+    if (outage)   // host array: validate (the device paths read no memory for these)
+        for (int32_t k = 0; k < K; ++k)
+            if (outage[k] < -1 || outage[k] >= p->d.L)
+                return pf::invalid("outage index outside [-1, n_line)");
     if (blocks_per_stage < 1) blocks_per_stage = 1;
     if (n_streams < 1) n_streams = 1;
     if (n_streams > 8) n_streams = 8;

@@ -13,7 +13,7 @@ import ctypes as C
 import numpy as np
 
 from . import _abi
-from ._abi import PF_LANES, check, lib, ptr
+from ._abi import PF_LANES, check, lib
 
 
 def _torch():
@@ -22,11 +22,44 @@ def _torch():
     return torch
 
 
-def _stream_ptr(stream) -> int:
+def _stream_ptr(stream, device=None) -> int:
+    """Raw cudaStream_t: ``stream`` (a torch stream or an int), else the
+    current stream of ``device``.  A torch stream of another device is
+    rejected."""
     torch = _torch()
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
+    if device is not None and hasattr(stream, "device") and stream.device != device:
+        raise ValueError(f"stream is on {stream.device}, the plan on {device}")
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _on_device(fn):
+    """Run a Plan method with the plan's device current: kernels launch, and
+    plan-owned staging is allocated, in the plan's context whatever device
+    the caller has current."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **k):
+        with _torch().cuda.device(self.device):
+            return fn(self, *a, **k)
+
+    return wrapped
+
+
+def _host(a, n: int, name: str, dtype=np.float64):
+    """Host array argument of the *_host entry points: C-contiguous, of
+    ``dtype``, at least ``n`` entries; returns its address (None passes)."""
+    if a is None:
+        return None
+    if not isinstance(a, np.ndarray):
+        raise ValueError(f"{name} must be a numpy array")
+    if a.dtype != dtype or not a.flags.c_contiguous:
+        raise ValueError(f"{name} must be a C-contiguous {np.dtype(dtype).name} array")
+    if a.size < n:
+        raise ValueError(f"{name} has {a.size} entries, expected >= {n}")
+    return a.ctypes.data
 
 
 def pinned_zeros(n: int):
@@ -100,7 +133,8 @@ class Plan:
 
     def close(self) -> None:
         if getattr(self, "_h", None):
-            lib().pf_plan_destroy(self._h)
+            with _torch().cuda.device(self.device):
+                lib().pf_plan_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -110,12 +144,14 @@ class Plan:
             pass
 
     # -- pattern ------------------------------------------------------------
+    @_on_device
     def pattern_csr(self):
         indptr = np.zeros(self.n_var + 1, np.int32)
         indices = np.zeros(max(self.nnz, 1), np.int32)
         check(lib().pf_plan_pattern_csr(self._h, indptr.ctypes.data, indices.ctypes.data))
         return indptr, indices[: self.nnz]
 
+    @_on_device
     def pattern_csc(self):
         indptr = np.zeros(self.n_var + 1, np.int32)
         indices = np.zeros(max(self.nnz, 1), np.int32)
@@ -140,6 +176,8 @@ class Plan:
         need = n if K == 0 else n_blocks(K) * PF_LANES * n
         if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
             raise ValueError(f"{name} must be a CUDA tensor")
+        if t.device != self.device:
+            raise ValueError(f"{name} is on {t.device}, the plan on {self.device}")
         if t.dtype != dtype or not t.is_contiguous():
             raise ValueError(f"{name} must be a contiguous {dtype} tensor")
         if t.numel() < need:
@@ -147,12 +185,14 @@ class Plan:
         return t.data_ptr()
 
     # -- evaluation (device pointers) -----------------------------------------
+    @_on_device
     def eval(self, y, g=None, jval=None, norm=None, stream=None) -> None:
         """Fused f+J of one grid: ``pf_eval``.  jval is CSR-ordered."""
         check(lib().pf_eval(self._h, self._dev(y, self.n_var, "y"), self._dev(g, self.n_var, "g"),
                             self._dev(jval, self.nnz, "jval"), self._dev(norm, 1, "norm"),
-                            _stream_ptr(stream)))
+                            _stream_ptr(stream, self.device)))
 
+    @_on_device
     def eval_batched(self, K: int, y, pq_p=None, pq_q=None, pv_p=None, outage=None, g=None,
                      jval=None, norms=None, stream=None) -> None:
         """K scenarios in the blocked layout: ``pf_eval_batched``."""
@@ -163,13 +203,16 @@ class Plan:
             self._dev(pv_p, self.n_pv, "pv_p", K),
             self._dev(outage, K, "outage", 0, torch.int32),
             self._dev(g, self.n_var, "g", K), self._dev(jval, self.nnz, "jval", K),
-            self._dev(norms, K, "norms"), _stream_ptr(stream)))
+            self._dev(norms, K, "norms"), _stream_ptr(stream, self.device)))
 
+    @_on_device
     def jac_to_csc(self, jcsr, jcsc, K: int = 0, stream=None) -> None:
         check(lib().pf_jac_to_csc(self._h, int(K), self._dev(jcsr, self.nnz, "jcsr", K),
-                                  self._dev(jcsc, self.nnz, "jcsc", K), _stream_ptr(stream)))
+                                  self._dev(jcsc, self.nnz, "jcsc", K),
+                                  _stream_ptr(stream, self.device)))
 
     # -- host-buffer drop-in ------------------------------------------------
+    @_on_device
     def eval_host(self, y: np.ndarray, g: np.ndarray | None = None,
                   jcsc: np.ndarray | None = None, norm: np.ndarray | None = None) -> None:
         """``pf_eval_host``: numpy in, numpy out (J in the reference's CSC order)."""
@@ -185,57 +228,78 @@ class Plan:
         check(lib().pf_eval_host(self._h, y.ctypes.data, chk(g, self.n_var, "g"),
                                  chk(jcsc, self.nnz, "jcsc"), chk(norm, 1, "norm")))
 
+    @_on_device
     def eval_batched_host(self, K: int, y, pq_p=None, pq_q=None, pv_p=None, outage=None,
                           g=None, jval=None, norms=None, blocks_per_stage: int = 1,
                           n_streams: int = 3) -> None:
-        """``pf_eval_batched_host``: host arrays (ideally pinned) in blocked layout."""
-        check(lib().pf_eval_batched_host(self._h, int(K), ptr(y), ptr(pq_p), ptr(pq_q),
-                                         ptr(pv_p), ptr(outage), ptr(g), ptr(jval), ptr(norms),
-                                         int(blocks_per_stage), int(n_streams)))
+        """``pf_eval_batched_host``: host arrays (ideally pinned) in blocked
+        layout.  Every array is checked (dtype, contiguity, size; outage
+        indices in [-1, n_line)) before any copy touches it."""
+        K = int(K)
+        if K < 0:
+            raise ValueError(f"K = {K} < 0")
+        lanes = n_blocks(K) * PF_LANES
+        if y is None:
+            raise ValueError("y is required")
+        args = [_host(y, lanes * self.n_var, "y"), _host(pq_p, lanes * self.n_pq, "pq_p"),
+                _host(pq_q, lanes * self.n_pq, "pq_q"), _host(pv_p, lanes * self.n_pv, "pv_p"),
+                _host(outage, K, "outage", np.int32), _host(g, lanes * self.n_var, "g"),
+                _host(jval, lanes * self.nnz, "jval"), _host(norms, K, "norms")]
+        if outage is not None and K and (outage[:K].min() < -1 or outage[:K].max() >= self.n_line):
+            raise ValueError(f"outage indices must lie in [-1, {self.n_line})")
+        check(lib().pf_eval_batched_host(self._h, K, *args, int(blocks_per_stage),
+                                         int(n_streams)))
 
     # -- per-model entry points -----------------------------------------------
+    @_on_device
     def line_injections(self, y, stream=None):
         """(ph, pk, qh, qk) device tensors (pflow residual.py:287-314)."""
         out = [self.empty(self.n_line) for _ in range(4)]
         check(lib().pf_line_injections(self._h, self._dev(y, self.n_var, "y"),
-                                       *[o.data_ptr() for o in out], _stream_ptr(stream)))
+                                       *[o.data_ptr() for o in out],
+                                       _stream_ptr(stream, self.device)))
         return tuple(o[: self.n_line] for o in out)
 
+    @_on_device
     def line_jacobian_slots(self, y, stream=None):
         """[16, n_line] line partials (pflow kernels.py:128-163)."""
         out = self.empty(16 * self.n_line)
         check(lib().pf_line_jacobian_slots(self._h, self._dev(y, self.n_var, "y"),
-                                           out.data_ptr(), _stream_ptr(stream)))
+                                           out.data_ptr(), _stream_ptr(stream, self.device)))
         return out[: 16 * self.n_line].view(16, self.n_line)
 
+    @_on_device
     def device_injections(self, y, stream=None):
         """Pool segments 4..14 of pflow residual.py:57."""
         n = 2 * self.n_pq + 3 * self.n_pv + 4 * self.n_slack + 2 * self.n_shunt
         out = self.empty(n)
         check(lib().pf_device_injections(self._h, self._dev(y, self.n_var, "y"), out.data_ptr(),
-                                         _stream_ptr(stream)))
+                                         _stream_ptr(stream, self.device)))
         return out[:n]
 
+    @_on_device
     def device_jacobian_slots(self, y, stream=None):
         n = 2 * self.n_pv + 4 * self.n_slack + 2 * self.n_shunt
         out = self.empty(n)
         check(lib().pf_device_jacobian_slots(self._h, self._dev(y, self.n_var, "y"),
-                                             out.data_ptr(), _stream_ptr(stream)))
+                                             out.data_ptr(), _stream_ptr(stream, self.device)))
         return out[:n]
 
 
 def join_rows(ptr_, split, idx, pool, out, stream=None) -> None:
     """Device row join (pflow kernels.py:265-274) on int32/float64 CUDA tensors."""
     n = out.numel()
-    check(lib().pf_join_rows(n, ptr_.data_ptr(), split.data_ptr(), idx.data_ptr(),
-                             pool.data_ptr(), out.data_ptr(), _stream_ptr(stream)))
+    with _torch().cuda.device(out.device):
+        check(lib().pf_join_rows(n, ptr_.data_ptr(), split.data_ptr(), idx.data_ptr(),
+                                 pool.data_ptr(), out.data_ptr(), _stream_ptr(stream, out.device)))
 
 
 def gather_sum(ptr_, idx, vals, out, stream=None) -> None:
     """Device duplicate-slot assembly (pflow kernels.py:277-282)."""
     n = out.numel()
-    check(lib().pf_gather_sum(n, ptr_.data_ptr(), idx.data_ptr(), vals.data_ptr(),
-                              out.data_ptr(), _stream_ptr(stream)))
+    with _torch().cuda.device(out.device):
+        check(lib().pf_gather_sum(n, ptr_.data_ptr(), idx.data_ptr(), vals.data_ptr(),
+                                  out.data_ptr(), _stream_ptr(stream, out.device)))
 
 
 def sincos(x, stream=None):
@@ -243,8 +307,9 @@ def sincos(x, stream=None):
     torch = _torch()
     x = x.contiguous()
     s, c = torch.empty_like(x), torch.empty_like(x)
-    check(lib().pf_sincos(x.numel(), x.data_ptr(), s.data_ptr(), c.data_ptr(),
-                          _stream_ptr(stream)))
+    with torch.cuda.device(x.device):
+        check(lib().pf_sincos(x.numel(), x.data_ptr(), s.data_ptr(), c.data_ptr(),
+                              _stream_ptr(stream, x.device)))
     return s, c
 
 

@@ -346,6 +346,42 @@ def test_errors_are_loud():
         plan.eval(torch.zeros(plan.n_var, dtype=torch.float32, device="cuda"))
     with pytest.raises(ValueError):
         plan.eval_host(np.zeros(plan.n_var - 1))
+    # host batched entry point: every array checked before any copy
+    from paper_2011_11880_b200.plan import to_blocked
+
+    K = 40
+    sb = synth.make_scenarios(s, K, seed=3)
+    y = to_blocked(sb.y.T)
+    lanes = 64
+    ok = dict(g=np.zeros(lanes * plan.n_var), jval=np.zeros(lanes * plan.nnz),
+              norms=np.zeros(K))
+    plan.eval_batched_host(K, y, outage=sb.outage.astype(np.int32), **ok)
+    for bad in (dict(ok, g=np.zeros(lanes * plan.n_var - 1)),           # undersized output
+                dict(ok, jval=np.zeros(lanes * plan.nnz, np.float32)),  # wrong dtype
+                dict(ok, norms=np.zeros((K, 2))[:, 0])):                # non-contiguous
+        with pytest.raises(ValueError):
+            plan.eval_batched_host(K, y, outage=sb.outage.astype(np.int32), **bad)
+    with pytest.raises(ValueError):
+        plan.eval_batched_host(K, y.astype(np.float32), **ok)
+    with pytest.raises(ValueError):
+        plan.eval_batched_host(K, y, outage=sb.outage.astype(np.int64), **ok)
+    for o in (plan.n_line, -2):
+        out = sb.outage.astype(np.int32)
+        out[5] = o
+        with pytest.raises(ValueError):
+            plan.eval_batched_host(K, y, outage=out, **ok)
+    # the device path reads no memory for an out-of-range outage: no outage
+    dy = torch.as_tensor(y, device="cuda")
+    res = []
+    for o in (-1, plan.n_line + 7, -5, 2 ** 31 - 1):
+        out = torch.full((K,), o, dtype=torch.int32, device="cuda")
+        g = plan.empty(plan.n_var, K)
+        plan.eval_batched(K, dy, outage=out, g=g)
+        res.append(g.cpu().numpy())
+    assert all(np.array_equal(r, res[0]) for r in res[1:])
+    # tensors on the wrong device / of the wrong kind are rejected
+    with pytest.raises(ValueError):
+        plan.eval(torch.zeros(plan.n_var, dtype=torch.float64))
 
 
 def test_deterministic_repeat():
