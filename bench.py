@@ -507,6 +507,20 @@ def run_gpu(args):
                           "restated in C (oracle/), one scenario per thread, workspace outputs"}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"error": repr(e)}
+        # the live reference beside the port (when pflow travelled here)
+        try:
+            from oracle import live  # cpu_baseline legs only
+
+            from paper_2011_11880_b200 import synth
+
+            pflow, why = live.import_pflow()
+            cfg = WORKLOADS[args.workload][0]
+            line["cpu_baseline_pflow"] = (
+                live.time_batched(pflow, synth.config_case(cfg, seed=cfg),
+                                  WORKLOADS[args.workload][1], SEED, threads, 4 * threads)
+                if pflow is not None else {"unavailable": why})
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline_pflow"] = {"error": repr(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -569,7 +583,8 @@ def _single_grid_config(dev, cfg: int, steps: int, cpu: bool = True) -> dict:
     from paper_2011_11880_b200.plan import Plan
     from paper_2011_11880_b200.system_model import build_system, random_state
 
-    s = build_system(synth.config_case(cfg, seed=cfg))
+    raw = synth.config_case(cfg, seed=cfg)
+    s = build_system(raw)
     plan = Plan(s, device=dev)
     _, static, _ = algorithmic_bytes(s, plan.nnz, 1)
     # single grid: base loads read from the plan's device parameters
@@ -665,7 +680,23 @@ def _single_grid_config(dev, cfg: int, steps: int, cpu: bool = True) -> dict:
             "batch100_kernel": "k_eval_staged<RES|JAC|NORM> (K = 100 states, one launch)",
             "n_var": plan.n_var, "nnz": plan.nnz, "kernel": "k_eval_single<RES|JAC|NORM>",
             "ctas": plan.single_chunks,
-            "cpu_baseline": single_cpu_baseline(s, y0) if cpu else None}
+            "cpu_baseline": single_cpu_baseline(s, y0) if cpu else None,
+            "cpu_baseline_pflow": single_pflow_baseline(raw, y0) if cpu else None}
+
+
+def single_pflow_baseline(raw, y0) -> dict | None:
+    """The live reference (pflow, Numba) timed beside the C port, when it is
+    importable here (baseline/_ref travels to the GPU box)."""
+    try:
+        from oracle import live  # cpu_baseline legs only
+
+        pflow, why = live.import_pflow()
+        if pflow is None:
+            return {"unavailable": why}
+        return live.time_single_grid(pflow, live.pflow_system(pflow, raw), y0,
+                                     os.cpu_count() or 1, min_seconds=0.3)
+    except Exception as e:  # noqa: BLE001
+        return {"error": repr(e)}
 
 
 def main():

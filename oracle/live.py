@@ -63,3 +63,120 @@ def pflow_fixture(pflow, name: str):
     """pflow's bundled MATPOWER fixture (cases/<name>.m) through pflow."""
     path = Path(pflow.__file__).resolve().parent / "cases" / f"{name}.m"
     return pflow.build_system(pflow.parse_case_file(path))
+
+
+# ---------------------------------------------------------------------------
+# live-pflow CPU baselines (bench.py's cpu_baseline_pflow legs)
+# ---------------------------------------------------------------------------
+
+def time_single_grid(pflow, psys, y, threads: int, min_seconds: float = 1.0) -> dict:
+    """pflow's own f+J (evaluate_residual + evaluate_jacobian on bound
+    workspaces) under each of its six workflows with ``threads`` pool
+    workers; warm-up discarded, median per f+J (the pflow/bench.py:82-90
+    method).  Returns the fastest and every workflow's median."""
+    import statistics
+    import time
+
+    import numpy as np
+
+    pflow.set_worker_count(max(threads, 6))     # wf4 needs >= 6 (workflow.py:209-212)
+    y = np.array(y, dtype=np.float64)
+    out = np.zeros(psys.n_var)
+    res_ws = pflow.ResidualWorkspace(psys)
+    jac_ws = pflow.symbolic_pattern(psys)
+    med = {}
+    for wf in range(1, 7):
+        cfg = pflow.workflow_config(wf, threads)
+        pflow.evaluate_residual(psys, y, cfg, out, res_ws)
+        pflow.evaluate_jacobian(psys, y, cfg, jac_ws)
+        times, t_start = [], time.perf_counter()
+        while len(times) < 5 or time.perf_counter() - t_start < min_seconds:
+            t0 = time.perf_counter()
+            pflow.evaluate_residual(psys, y, cfg, out, res_ws)
+            pflow.evaluate_jacobian(psys, y, cfg, jac_ws)
+            times.append(time.perf_counter() - t0)
+        med[wf] = statistics.median(times)
+    best = min(med, key=med.get)
+    return {"value": 1.0 / med[best], "unit": "evals/s", "us_per_eval": med[best] * 1e6,
+            "wf": best, "cores": threads if best in (2, 3, 4, 6) else 1,
+            "kind": "reference",
+            "per_workflow_us": {str(k): v * 1e6 for k, v in med.items()},
+            "sample": f"live pflow {pflow.__version__} (Numba), evaluate_residual + "
+                      "evaluate_jacobian on bound workspaces, each of wf1-6, median per f+J, "
+                      "fastest reported"}
+
+
+def _scenario_worker(args):
+    """One process of the batched baseline: its own PowerSystem, mutated in
+    place per scenario, wf5 on one thread
+    (PAPER.md:416-422).  Returns (scenarios done, seconds)."""
+    import time
+
+    import numpy as np
+
+    text, name, K, seed, lo, hi, wf = args
+    pflow, why = import_pflow()
+    if pflow is None:
+        raise RuntimeError(why)
+    from paper_2011_11880_b200 import synth
+
+    psys = pflow.build_system(pflow.parse_case(text, name=name))
+    sb = synth.make_scenarios(psys, K, seed)
+    pflow.set_worker_count(1)
+    cfg = pflow.workflow_config(wf, 1)
+    out = np.zeros(psys.n_var)
+    res_ws = pflow.ResidualWorkspace(psys)
+    jac_ws = pflow.symbolic_pattern(psys)
+    ln, pq, pv = psys.lines, psys.pq, psys.pv
+    coef = [ln.gl, ln.bl, ln.gl2, ln.bl2, ln.g_self_h, ln.b_self_h, ln.g_self_k, ln.b_self_k]
+    p0, q0, v0 = pq.p0.copy(), pq.q0.copy(), pv.p0.copy()
+
+    def one(k):
+        y = np.ascontiguousarray(sb.y[:, k])
+        pq.p0[:] = sb.pq_p[:, k]
+        pq.q0[:] = sb.pq_q[:, k]
+        pv.p0[:] = sb.pv_p[:, k]
+        o = int(sb.outage[k])
+        saved = [c[o] for c in coef] if o >= 0 else None
+        if o >= 0:
+            for c in coef:
+                c[o] = 0.0
+        pflow.evaluate_residual(psys, y, cfg, out, res_ws)
+        pflow.evaluate_jacobian(psys, y, cfg, jac_ws)
+        if o >= 0:
+            for c, v in zip(coef, saved):
+                c[o] = v
+        pq.p0[:], pq.q0[:], pv.p0[:] = p0, q0, v0
+
+    one(lo)                                   # warm-up (JIT / cache load)
+    t0 = time.perf_counter()
+    for k in range(lo, hi):
+        one(k)
+    return hi - lo, time.perf_counter() - t0
+
+
+def time_batched(pflow, raw_case, K: int, seed: int, procs: int, n_scen: int,
+                 wf: int = 5) -> dict:
+    """The paper's recommended batch: independent single-threaded wf5 jobs in
+    parallel processes, one per core, over the first
+    ``n_scen`` of the workload's K scenarios (a bounded sample)."""
+    import multiprocessing as mp
+
+    from paper_2011_11880_b200 import case as C
+
+    text = C.write_case(raw_case)
+    # populate Numba's on-disk cache once before the workers load it
+    _scenario_worker((text, raw_case.name, K, seed, 0, 1, wf))
+    n_scen = min(n_scen, K)
+    cuts = [n_scen * r // procs for r in range(procs + 1)]
+    jobs = [(text, raw_case.name, K, seed, cuts[r], cuts[r + 1], wf) for r in range(procs)
+            if cuts[r + 1] > cuts[r]]
+    with mp.get_context("spawn").Pool(len(jobs)) as pool:
+        res = pool.map(_scenario_worker, jobs)
+    done = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": done / wall, "unit": "evals/s", "cores": len(jobs), "kind": "reference",
+            "wf": wf,
+            "sample": f"live pflow {pflow.__version__} (Numba): {done} of the {K} scenarios, "
+                      f"{len(jobs)} processes x wf{wf} single-threaded, each mutating its own "
+                      "PowerSystem per scenario; evals / slowest process's time"}
