@@ -231,6 +231,11 @@ PF_API int pf_lu_residual(int32_t K, int32_t n, int32_t nnz, const int32_t* csr_
 /* Number of kernels this library has launched (process-wide counter). */
 PF_API int64_t pf_launch_count(void);
 
+/* Number of device allocations this library has made (process-wide counter):
+ * plan creation and the first host-buffer call per plan allocate; evaluations
+ * never do (SPEC.md:197, 457 allocation contract). */
+PF_API int64_t pf_alloc_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,7 @@ _SIGS = {
     "pf_lu_residual": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP, _VP, _VP,
                                  _VP]),
     "pf_launch_count": (C.c_int64, []),
+    "pf_alloc_count": (C.c_int64, []),
 }
 
 EXPORTED = tuple(_SIGS)

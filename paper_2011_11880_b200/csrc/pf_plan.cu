@@ -22,6 +22,15 @@ namespace pf {
 
 static thread_local std::string g_err;
 static std::atomic<int64_t> g_launches{0};
+static std::atomic<int64_t> g_allocs{0};
+
+// Every device allocation of the library goes through here (counted: the
+// zero-allocation steady state of SPEC.md:197 / 457 is asserted in tests).
+template <class T>
+static cudaError_t dmalloc(T** p, size_t bytes) {
+    g_allocs.fetch_add(1, std::memory_order_relaxed);
+    return cudaMalloc((void**)p, bytes);
+}
 
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -290,7 +299,7 @@ struct Scratch {
     template <class T>
     cudaError_t alloc(T** p, int64_t n) {
         *p = nullptr;
-        cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1));
+        cudaError_t e = dmalloc(p, sizeof(T) * (size_t)(n > 0 ? n : 1));
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }
@@ -300,7 +309,7 @@ template <class T>
 cudaError_t owned_alloc(pf_plan* P, T** p, int64_t n) {
     *p = nullptr;
     if (P->n_owned >= (int)(sizeof(P->owned) / sizeof(P->owned[0]))) return cudaErrorMemoryAllocation;
-    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1));
+    cudaError_t e = dmalloc(p, sizeof(T) * (size_t)(n > 0 ? n : 1));
     if (e == cudaSuccess) P->owned[P->n_owned++] = *p;
     return e;
 }
@@ -846,6 +855,8 @@ int pf_version(void) { return 1; }
 
 int64_t pf_launch_count(void) { return pf::g_launches.load(); }
 
+int64_t pf_alloc_count(void) { return pf::g_allocs.load(); }
+
 int pf_plan_create(const pf_topology* topo, pf_plan** out) {
     if (!out) return pf::invalid("out is NULL");
     *out = nullptr;
@@ -949,11 +960,11 @@ int pf_eval_host(pf_plan* p, const double* y, double* g, double* jcsc, double* n
     const DevicePlan& d = p->d;
     if (!p->s_stream) {
         PF_CUDA(cudaStreamCreateWithFlags(&p->s_stream, cudaStreamNonBlocking));
-        PF_CUDA(cudaMalloc(&p->s_y, sizeof(double) * (size_t)(d.n_var + 1)));
-        PF_CUDA(cudaMalloc(&p->s_g, sizeof(double) * (size_t)(d.n_var + 1)));
-        PF_CUDA(cudaMalloc(&p->s_j, sizeof(double) * (size_t)(d.nnz + 1)));
-        PF_CUDA(cudaMalloc(&p->s_jc, sizeof(double) * (size_t)(d.nnz + 1)));
-        PF_CUDA(cudaMalloc(&p->s_norm, sizeof(double)));
+        PF_CUDA(pf::dmalloc(&p->s_y, sizeof(double) * (size_t)(d.n_var + 1)));
+        PF_CUDA(pf::dmalloc(&p->s_g, sizeof(double) * (size_t)(d.n_var + 1)));
+        PF_CUDA(pf::dmalloc(&p->s_j, sizeof(double) * (size_t)(d.nnz + 1)));
+        PF_CUDA(pf::dmalloc(&p->s_jc, sizeof(double) * (size_t)(d.nnz + 1)));
+        PF_CUDA(pf::dmalloc(&p->s_norm, sizeof(double)));
     }
     cudaStream_t st = p->s_stream;
     PF_CUDA(cudaMemcpyAsync(p->s_y, y, sizeof(double) * (size_t)d.n_var, cudaMemcpyHostToDevice, st));
@@ -998,14 +1009,14 @@ int pf_eval_batched_host(pf_plan* p, int32_t K, const double* y, const double* p
         const size_t lanes = (size_t)blocks_per_stage * PF_LANES;
         for (int s = 0; s < n_streams; ++s) {
             PF_CUDA(cudaStreamCreateWithFlags(&b.streams[s], cudaStreamNonBlocking));
-            PF_CUDA(cudaMalloc(&b.y[s], sizeof(double) * lanes * (size_t)d.n_var));
-            PF_CUDA(cudaMalloc(&b.g[s], sizeof(double) * lanes * (size_t)d.n_var));
-            PF_CUDA(cudaMalloc(&b.j[s], sizeof(double) * lanes * (size_t)(d.nnz + 1)));
-            PF_CUDA(cudaMalloc(&b.pq_p[s], sizeof(double) * lanes * (size_t)(d.P + 1)));
-            PF_CUDA(cudaMalloc(&b.pq_q[s], sizeof(double) * lanes * (size_t)(d.P + 1)));
-            PF_CUDA(cudaMalloc(&b.pv_p[s], sizeof(double) * lanes * (size_t)(d.G + 1)));
-            PF_CUDA(cudaMalloc(&b.outage[s], sizeof(int32_t) * lanes));
-            PF_CUDA(cudaMalloc(&b.norms[s], sizeof(double) * lanes));
+            PF_CUDA(pf::dmalloc(&b.y[s], sizeof(double) * lanes * (size_t)d.n_var));
+            PF_CUDA(pf::dmalloc(&b.g[s], sizeof(double) * lanes * (size_t)d.n_var));
+            PF_CUDA(pf::dmalloc(&b.j[s], sizeof(double) * lanes * (size_t)(d.nnz + 1)));
+            PF_CUDA(pf::dmalloc(&b.pq_p[s], sizeof(double) * lanes * (size_t)(d.P + 1)));
+            PF_CUDA(pf::dmalloc(&b.pq_q[s], sizeof(double) * lanes * (size_t)(d.P + 1)));
+            PF_CUDA(pf::dmalloc(&b.pv_p[s], sizeof(double) * lanes * (size_t)(d.G + 1)));
+            PF_CUDA(pf::dmalloc(&b.outage[s], sizeof(int32_t) * lanes));
+            PF_CUDA(pf::dmalloc(&b.norms[s], sizeof(double) * lanes));
             b.n_streams = s + 1;
         }
         b.blocks = blocks_per_stage;

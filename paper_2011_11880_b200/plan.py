@@ -316,3 +316,8 @@ def sincos(x, stream=None):
 def launch_count() -> int:
     """Kernels libpfgpu has launched in this process."""
     return int(lib().pf_launch_count())
+
+
+def alloc_count() -> int:
+    """Device allocations libpfgpu has made in this process."""
+    return int(lib().pf_alloc_count())
