@@ -138,7 +138,10 @@ def lib():
         handle = C.CDLL(str(path))
     except OSError as e:
         raise RuntimeError(f"failed to load {path}: {e}") from e
+    partial = os.environ.get("PFGPU_LIB_PARTIAL") == "1"   # dev A/B of older builds only
     for name, (res, args) in _SIGS.items():
+        if partial and not hasattr(handle, name):
+            continue
         fn = getattr(handle, name)
         fn.restype = res
         fn.argtypes = args

@@ -1086,24 +1086,26 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
     // barrier (it is not read before).
     const int4 c0 = __ldg(d.sg_chunk + 2 * blockIdx.x);
     const int4 c1 = __ldg(d.sg_chunk + 2 * blockIdx.x + 1);
-    // trig table: 16-byte cp.async copies straight into shared memory (no
-    // registers held across the plan loads); waited for at the first barrier
     constexpr int TAB16 = PF_TRIG_N * 4 / 2;
     static_assert(TAB16 <= 2 * SG_THREADS, "trig table staging");
-    {
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_tab);
-        for (int c = t; c < TAB16; c += SG_THREADS)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * c),
-                         "l"(pf_trig_tab + 2 * c) : "memory");
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    }
+// trig table: two 16-byte loads per thread into registers now, stored to
+    // shared memory before the first barrier (cp.async staging instead cost
+    // 1.4 us per evaluation in the graph: its completion wait lands after
+    // griddepcontrol.wait, on the critical path)
+    double2 tv[2];
+    for (int r = 0; r < 2; ++r)
+        tv[r] = t + r * SG_THREADS < TAB16
+                    ? __ldg(reinterpret_cast<const double2*>(pf_trig_tab) + t + r * SG_THREADS)
+                    : make_double2(0.0, 0.0);
     const double* tab = s_tab;
     const int32_t b0 = c0.x, b1 = c0.y & ~SG_BIG, E0 = c0.z, E1 = c0.w;
     const Scen<1> A{y, nullptr, nullptr, nullptr, g, jv, -1};
     unsigned long long nrm = 0;
     if (c0.y & SG_BIG) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        asm volatile("cp.async.wait_all;" ::: "memory");
+        for (int r = 0; r < 2; ++r)
+            if (t + r * SG_THREADS < TAB16)
+                reinterpret_cast<double2*>(s_tab)[t + r * SG_THREADS] = tv[r];
         __syncthreads();
         if (t == 0) nrm = eval_bus<MODE, 1>(d, tab, b0, A, 0, -1);
     } else {
@@ -1144,6 +1146,9 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             single_dev_plan(src, d, t0, nd > 0, src.dv0, src.a0, src.b0, src.c0, src.d0);
             single_dev_plan(src, d, t0 + 1, nd > 1, src.dv1, src.a1, src.b1, src.c1, src.d1);
         }
+        for (int r = 0; r < 2; ++r)
+            if (t + r * SG_THREADS < TAB16)
+                reinterpret_cast<double2*>(s_tab)[t + r * SG_THREADS] = tv[r];
         // state: after the preceding kernel's writes are visible
         asm volatile("griddepcontrol.wait;" ::: "memory");
         double tja = 0.0, wja = 0.0, tjb = 0.0, wjb = 0.0;
@@ -1164,7 +1169,6 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             bv[t] = src.vi;
             bnb[t] = src.h0.z;
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         auto incidence = [&](int32_t e, int4 r, double4 c, double tj, double wj) {   // phase A
             const int32_t o = r.y & SG_FIELD_MASK;
