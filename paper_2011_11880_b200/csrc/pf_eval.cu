@@ -887,6 +887,50 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             evaluate(k, blk, (item - blk * n_groups) * W + q % W);
         }
     } else {
+#ifdef PF_X_CONTIG
+        // CTA-contiguous groups: in every scenario block CTA c takes the
+        // groups [lo, hi) of an even split, so its J and g rows form one long
+        // ascending stream per block instead of W-bus windows G groups apart.
+        const int32_t lo = (int32_t)(((int64_t)n_groups * blockIdx.x) / stride);
+        const int32_t nc = (int32_t)(((int64_t)n_groups * (blockIdx.x + 1)) / stride) - lo;
+        const int32_t nblk = n_groups ? n_items / n_groups : 0;
+        const int32_t steps = nc * nblk;
+        auto cword = [&](int32_t k) -> int32_t {
+            if (k >= steps) return -1;
+            const int32_t b = k / nc;
+            const int32_t slot = (lo + (k - b * nc)) * W + warp;
+            if (slot >= d.N) return -1;
+            return __ldg(reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
+                         ((lane + 2) & 15));
+        };
+        auto cissue = [&](int32_t k, int32_t rw, uint32_t sb) {
+            if (k < steps && __shfl_sync(0xffffffffu, rw, 14) >= 0) {
+                const int32_t bb = k / nc;
+                if (bb != s_sblk[warp]) {
+                    __syncwarp();
+                    if (lane == 0) s_sblk[warp] = bb;
+                    if (lane < 4) {
+                        const double* a = lane == 0 ? y : lane == 1 ? pq_p : lane == 2 ? pq_q : pv_p;
+                        const int64_t n = lane == 0 ? d.n_var : lane == 3 ? d.G : d.P;
+                        s_base[warp][lane] = a ? a + (int64_t)bb * n * PF_LANES : nullptr;
+                    }
+                    __syncwarp();
+                }
+                stage_item(sb, rw, d.ws_pkt, s_base[warp], lane);
+            } else {
+                cp_async_commit();
+            }
+        };
+        cissue(0, cword(0), slots_u32);
+        int32_t rw_next = cword(1);
+        for (int32_t k = 0; k < steps; ++k) {
+            const int32_t blk = k / nc;
+            if (blk != cur) enter_block(blk);
+            cissue(k + 1, rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
+            rw_next = cword(k + 2);
+            evaluate(k, blk, (lo + (k - blk * nc)) * W + warp);
+        }
+#else
         // prologue: item 0's copies in flight, item 1's record in a register
         issue(blockIdx.x, rec_word(blockIdx.x), slots_u32);
         int32_t rw_next = rec_word(blockIdx.x + stride);
@@ -901,6 +945,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             rw_next = rec_word(item + 2 * stride);
             evaluate(k, blk, (item - blk * n_groups) * W + warp);
         }
+#endif
     }
     cp_async_wait<0>();
     if (cur >= 0) flush(cur);
