@@ -659,6 +659,19 @@ def _single_grid_config(dev, cfg: int, steps: int, cpu: bool = True) -> dict:
         if k >= 3:
             drop.append(time.perf_counter() - t0)
     med_d = statistics.median(drop)
+    # the fused pair (JacobianWorkspace(..., residual_ws=rws)): one upload and
+    # one launch per Newton iteration, as pflow's newton_solve calls them
+    rws_f = ResidualWorkspace(s, plan)
+    jws_f = JacobianWorkspace(s, plan, residual_ws=rws_f)
+    rws_f.bind(y_h, g_h)
+    drop_f = []
+    for k in range(3 + max(steps, 10)):
+        t0 = time.perf_counter()
+        rws_f.run(y_h)
+        jws_f.run(y_h)
+        if k >= 3:
+            drop_f.append(time.perf_counter() - t0)
+    med_f = statistics.median(drop_f)
     # per state: y, g, J, norm; the plan's static data once per launch
     bytes_b = 100 * (16 * s.n_var + 8 * plan.nnz + 8) + static + 16 * len(s.pq) + 8 * len(s.pv)
     med_b = statistics.median(bat)
@@ -675,6 +688,9 @@ def _single_grid_config(dev, cfg: int, steps: int, cpu: bool = True) -> dict:
             "dropin_us_per_eval": med_d * 1e6, "dropin_evals_per_s": 1.0 / med_d,
             "dropin_api": "ResidualWorkspace.run + JacobianWorkspace.run (numpy y, numpy g, "
                           "scipy CSC J; host copies included)",
+            "dropin_fused_us_per_eval": med_f * 1e6, "dropin_fused_evals_per_s": 1.0 / med_f,
+            "dropin_fused_api": "the same pair fused (JacobianWorkspace(..., residual_ws=rws)): "
+                                "one upload of y and one launch for g and J",
             "batch100_us_per_eval": med_b * 1e3, "batch100_evals_per_s": 1e3 / med_b,
             "batch100_frac": bytes_b / (med_b * 100 / 1e3) / 1e9 / peak,
             "batch100_kernel": "k_eval_staged<RES|JAC|NORM> (K = 100 states, one launch)",

@@ -20,8 +20,19 @@ from .residual import ResidualWorkspace, evaluate_residual
 class JacobianWorkspace:
     """Fixed pattern + assembled CSC matrix for one system (pflow/jacobian.py:39-176)."""
 
-    def __init__(self, sys, plan: Plan | None = None):
+    def __init__(self, sys, plan: Plan | None = None, residual_ws: ResidualWorkspace | None = None):
+        """``residual_ws`` (optional) fuses the pair: its ``run(y)`` then
+        evaluates g and J in one upload and one launch, and this
+        workspace's next ``run`` with the same y object returns that J
+        without evaluating again -- the call pattern of pflow's
+        newton_solve (newton.py:81, 97), which leaves y untouched between
+        the two.  A caller that modifies y in place between the two calls
+        must not pair the workspaces."""
         self.sys = sys
+        if residual_ws is not None:
+            if plan is not None and plan is not residual_ws.plan:
+                raise ValueError("a fused pair must share one plan")
+            plan = residual_ws.plan
         self.plan = plan if plan is not None else Plan(sys)
         n = self.plan.n_var
         indptr, indices, perm = self.plan.pattern_csc()
@@ -34,6 +45,9 @@ class JacobianWorkspace:
             self.csc.data = data
         self.csc_perm = perm
         self._bound = None
+        self._fresh_for = None   # id(y) whose J the paired residual run left in csc
+        if residual_ws is not None:
+            residual_ws._paired = self
 
     def pattern_csr(self):
         """(indptr, indices) of the device CSR pattern (== csc.tocsr())."""
@@ -49,6 +63,10 @@ class JacobianWorkspace:
 
     def run(self, y, cfg=None) -> sp.csc_matrix:
         self.bind(y, cfg)
+        if self._fresh_for is not None and self._fresh_for == id(y):
+            self._fresh_for = None          # J of this y came with the residual run
+            return self.csc
+        self._fresh_for = None
         self.plan.eval_host(y, jcsc=self.csc.data)
         return self.csc
 

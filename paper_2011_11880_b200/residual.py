@@ -29,6 +29,7 @@ class ResidualWorkspace:
         self._pinned, self.residual = pinned_zeros(self.n_eq)   # page-locked: one DMA per run
         self._bound = None
         self._out = None
+        self._paired = None   # a JacobianWorkspace fused with this one (jacobian.py)
 
     def bind(self, y, out, cfg=None):
         """Validate and remember the output buffer (pflow/residual.py:129-144)."""
@@ -49,7 +50,14 @@ class ResidualWorkspace:
 
     def run(self, y, cfg=None):
         out = self.bind(y, self._out, cfg)
-        self.plan.eval_host(y, g=out)
+        jws = self._paired
+        if jws is not None:
+            # fused: one upload of y and one launch give g and J; the paired
+            # workspace returns this J for the same y object (see jacobian.py)
+            self.plan.eval_host(y, g=out, jcsc=jws.csc.data)
+            jws._fresh_for = id(y)
+        else:
+            self.plan.eval_host(y, g=out)
         return out
 
 

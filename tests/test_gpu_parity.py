@@ -129,6 +129,21 @@ def test_host_dropin_workspaces(gfx):
         assert_parity(csc.data, d["j_wf1"][i], "host J")
     with pytest.raises(ValueError):
         rws.run(np.zeros(plan.n_var + 1), None)
+    # fused pair: the residual run evaluates J too; the Jacobian run of the
+    # same y object returns it, any other y is evaluated afresh
+    rf = ResidualWorkspace(s, plan)
+    jf = JacobianWorkspace(s, plan, residual_ws=rf)
+    for i, y in enumerate(d["ys"]):
+        y = y.copy()
+        g = evaluate_residual(s, y, None, rf.residual, rf)
+        csc = evaluate_jacobian(s, y, None, jf)
+        assert_parity(g, d["g_wf1"][i], "fused g")
+        assert_parity(csc.data, d["j_wf1"][i], "fused J")
+        y2 = d["ys"][(i + 1) % len(d["ys"])].copy()
+        assert_parity(evaluate_jacobian(s, y2, None, jf).data,
+                      d["j_wf1"][(i + 1) % len(d["ys"])], "fused J, other y")
+    with pytest.raises(ValueError):
+        JacobianWorkspace(s, _plan(s), residual_ws=rf)
     with pytest.raises(ValueError):
         evaluate_jacobian(build_system(synth.synth_case(3, 3, seed=0, pq_frac=0.5)), d["ys"][0],
                           None, jws)

@@ -42,13 +42,17 @@ def _systems(pflow):
     return out
 
 
-def test_pflow_newton_solve_with_gpu_workspaces(pflow):
+@pytest.mark.parametrize("fused", [False, True])
+def test_pflow_newton_solve_with_gpu_workspaces(pflow, fused):
+    """fused: JacobianWorkspace(..., residual_ws=rws) -- each Newton
+    iteration's residual call also evaluates J in the same launch."""
     from paper_2011_11880_b200.jacobian import JacobianWorkspace
     from paper_2011_11880_b200.residual import ResidualWorkspace
 
     for name, psys in _systems(pflow):
         opts = pflow.NewtonOptions()
-        rws, jws = ResidualWorkspace(psys), JacobianWorkspace(psys)
+        rws = ResidualWorkspace(psys)
+        jws = JacobianWorkspace(psys, residual_ws=rws) if fused else JacobianWorkspace(psys)
         assert jws.sys is psys
         ref = pflow.newton_solve(psys, pflow.flat_start(psys), opts)
         got = pflow.newton_solve(psys, pflow.flat_start(psys), opts, residual_ws=rws,
