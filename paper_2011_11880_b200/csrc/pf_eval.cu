@@ -342,12 +342,25 @@ struct GlobalSrc {
 
 // One bus for one scenario (S = PF_LANES: batched lane; S = 1: single grid),
 // operands from `src` (global memory or a shared-memory staging slot).
-template <int MODE, int S, class Src, class JW>
+// Residual writer: every row straight to g (lane stride S).  (Staging the
+// single-grid chunk's g_p / g_q rows in shared memory and copying them out
+// after the norm measured 0.1 us slower per evaluation.)
+template <int S>
+struct GlobalG {
+    double* g;   // lane's view: row r at g[r * S]
+    __device__ __forceinline__ void pq(int32_t i, int32_t N, double p, double q) const {
+        st_out(g + i * S, p);
+        st_out(g + (N + i) * S, q);
+    }
+    __device__ __forceinline__ void row(int32_t r, double v) const { st_out(g + r * S, v); }
+};
+
+template <int MODE, int S, class Src, class JW, class GW = GlobalG<S>>
 __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, const double* tab,
                                                            const int32_t i, const Src& src,
                                                            const Scen<S>& A, const int32_t ln,
                                                            const int32_t out_l, const JW& jw,
-                                                           const bool ochk = true) {
+                                                           const bool ochk, const GW gw) {
     const int32_t N = d.N;
     const int4 br = src.hdr0();
     const int4 rng = src.hdr1();
@@ -419,7 +432,7 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
             acc_q += gb();
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - gc());
-                if (MODE & RES) st_out(A.g + ln + row * S, gv);
+                if (MODE & RES) gw.row(row, gv);
                 nrm = max(nrm, abs_bits(gv));
             }
             if (MODE & JAC) {
@@ -437,8 +450,8 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 const double gv = 0.0 + (v_i - gc());
                 const double gt = 0.0 + (th_i - gd());
                 if (MODE & RES) {
-                    st_out(A.g + ln + row_v * S, gv);
-                    st_out(A.g + ln + row_t * S, gt);
+                    gw.row(row_v, gv);
+                    gw.row(row_t, gt);
                 }
                 nrm = max(nrm, max(abs_bits(gv), abs_bits(gt)));
             }
@@ -477,8 +490,7 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
     }
 
     if (MODE & RES) {
-        st_out(A.g + ln + i * S, acc_p);
-        st_out(A.g + ln + (N + i) * S, acc_q);
+        gw.pq(i, N, acc_p, acc_q);
     }
     nrm = max(nrm, max(abs_bits(acc_p), abs_bits(acc_q)));
     if (MODE & JAC) {
@@ -500,7 +512,8 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
                                                        const int32_t ln, const int32_t out_l) {
     GlobalSrc<S> src{d, A, A.y + ln, i, ln};
     return eval_bus_src<MODE, S>(d, tab, i, src, A, ln, out_l,
-                                 GlobalJ<S>{A.j ? A.j + ln : nullptr});
+                                 GlobalJ<S>{A.j ? A.j + ln : nullptr}, true,
+                                 GlobalG<S>{A.g ? A.g + ln : nullptr});
 }
 
 // Batched, persistent: gridDim.x CTAs (a few per SM) stride over work items
@@ -906,7 +919,8 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
                                 sbu + WS_ROWS * WS_ROW_BYTES, cnt.x, cnt.y};
             nrm = max(nrm, eval_bus_src<MODE, PF_LANES>(
                                d, tab, cnt.z, src, A, lane, out_l,
-                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk));
+                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk,
+                               GlobalG<PF_LANES>{A.g ? A.g + lane : nullptr}));
         }
         __syncwarp();         // slot reads done before it is refilled
     };
@@ -1166,6 +1180,22 @@ __device__ __forceinline__ unsigned long long single_norm(const DevicePlan& d,
     return nrm;
 }
 
+#ifdef PF_X_TRACE
+// dev probe (scripts/dbg/sg_trace.py): %globaltimer at phase boundaries of
+// every CTA, thread 0's view (after each barrier every thread is there)
+__device__ unsigned long long g_sg_trace[4096 * 8];
+__device__ __forceinline__ void sg_stamp(int k) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_sg_trace[blockIdx.x * 8 + k] = t;
+    }
+}
+#define SG_STAMP(k) sg_stamp(k)
+#else
+#define SG_STAMP(k)
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const DevicePlan d,
                                                             const double* __restrict__ y,
@@ -1182,6 +1212,7 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
     // its griddepcontrol.wait, after which everything the preceding kernel
     // wrote (y included, whoever produced it) is visible.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    SG_STAMP(0);
     // Every global access is a ~0.5 us round trip here (one wave, one
     // dependent chain per CTA), so loads are issued level by level: chunk
     // record and trig table first, then everything that depends only on
@@ -1239,7 +1270,11 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             ra = __ldg(d.sg_inc + ea);
             ca = ldg4(d.inc_coef + ea);
         }
-        if (eb < E1) rb = __ldg(d.sg_inc + eb);
+        double4 cb_reg = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (eb < E1) {
+            rb = __ldg(d.sg_inc + eb);
+            cb_reg = ldg4(d.inc_coef + eb);
+        }
         SingleSrc src{{d, A, y, i, 0}, fold, dupv, E0, make_int4(0, 0, 0, 0),
                       make_int4(0, 0, 0, 0), 0.0, 0.0};
         if (own) {
@@ -1252,8 +1287,18 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         for (int r = 0; r < 2; ++r)
             if (t + r * SG_THREADS < TAB16)
                 reinterpret_cast<double2*>(s_tab)[t + r * SG_THREADS] = tv[r];
+        // the second incidence's coefficients wait in its own fold slot (free
+        // until phase A writes it): loaded now, before griddepcontrol.wait,
+        // instead of a global round trip inside phase A
+        if (eb < E1) {
+            double2* cs = reinterpret_cast<double2*>(fold + 6 * (eb - E0));
+            cs[0] = make_double2(cb_reg.x, cb_reg.y);
+            cs[1] = make_double2(cb_reg.z, cb_reg.w);
+        }
         // state: after the preceding kernel's writes are visible
+        SG_STAMP(1);
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        SG_STAMP(2);
         double tja = 0.0, wja = 0.0, tjb = 0.0, wjb = 0.0;
         if (ea < E1) {
             tja = __ldg(y + ra.x);
@@ -1273,6 +1318,7 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             bnb[t] = src.h0.z;
         }
         __syncthreads();
+        SG_STAMP(3);
         auto incidence = [&](int32_t e, int4 r, double4 c, double tj, double wj) {   // phase A
             const int32_t o = r.y & SG_FIELD_MASK;
             const int4 m = make_int4(r.x, -1, r.y & KSIDE, 0);
@@ -1297,20 +1343,29 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
             }
         };
         if (ea < E1) incidence(ea, ra, ca, tja, wja);
-        if (eb < E1) incidence(eb, rb, ldg4(d.inc_coef + eb), tjb, wjb);
+        if (eb < E1) {
+            const double2* cs = reinterpret_cast<const double2*>(fold + 6 * (eb - E0));
+            const double2 c01 = cs[0], c23 = cs[1];
+            incidence(eb, rb, make_double4(c01.x, c01.y, c23.x, c23.y), tjb, wjb);
+        }
         __syncthreads();
+        SG_STAMP(4);
         if (own)   // phase B
             nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1,
-                                        StagedJ{jpb, jqb, jv, c1.x, c1.y, c1.z, c1.w});
+                                        StagedJ{jpb, jqb, jv, c1.x, c1.y, c1.z, c1.w}, true,
+                                        GlobalG<1>{g});
         if (MODE & (JAC | NORM)) __syncthreads();
+        SG_STAMP(5);
         if (MODE & JAC) {   // staged rows out: one TMA bulk copy per range
             if (t == 0) bulk_out(jv + c1.x, jpb, lp);
             if (t == 32) bulk_out(jv + c1.z, jqb, lq);
         }
         if (MODE & NORM) nrm = single_norm(d, nrm, red, norm);
+        SG_STAMP(6);
         if (MODE & JAC) {
             if (t == 0 || t == 32) bulk_wait();   // smem must outlive the copy's reads
         }
+        SG_STAMP(7);
         return;
     }
     if (MODE & NORM) {
@@ -1838,3 +1893,9 @@ cudaError_t launch_sincos(int64_t n, const double* x, double* s, double* c, cuda
 }
 
 }  // namespace pf
+
+#ifdef PF_X_TRACE
+extern "C" __attribute__((visibility("default"))) int pf_debug_sg_trace(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, pf::g_sg_trace, sizeof(unsigned long long) * 4096 * 8);
+}
+#endif
