@@ -342,25 +342,12 @@ struct GlobalSrc {
 
 // One bus for one scenario (S = PF_LANES: batched lane; S = 1: single grid),
 // operands from `src` (global memory or a shared-memory staging slot).
-// Residual writer: every row straight to g (lane stride S).  (Staging the
-// single-grid chunk's g_p / g_q rows in shared memory and copying them out
-// after the norm measured 0.1 us slower per evaluation.)
-template <int S>
-struct GlobalG {
-    double* g;   // lane's view: row r at g[r * S]
-    __device__ __forceinline__ void pq(int32_t i, int32_t N, double p, double q) const {
-        st_out(g + i * S, p);
-        st_out(g + (N + i) * S, q);
-    }
-    __device__ __forceinline__ void row(int32_t r, double v) const { st_out(g + r * S, v); }
-};
-
-template <int MODE, int S, class Src, class JW, class GW = GlobalG<S>>
+template <int MODE, int S, class Src, class JW>
 __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, const double* tab,
                                                            const int32_t i, const Src& src,
                                                            const Scen<S>& A, const int32_t ln,
                                                            const int32_t out_l, const JW& jw,
-                                                           const bool ochk, const GW gw) {
+                                                           const bool ochk = true) {
     const int32_t N = d.N;
     const int4 br = src.hdr0();
     const int4 rng = src.hdr1();
@@ -432,7 +419,7 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
             acc_q += gb();
             if (MODE & (RES | NORM)) {
                 const double gv = 0.0 + (v_i - gc());
-                if (MODE & RES) gw.row(row, gv);
+                if (MODE & RES) st_out(A.g + ln + row * S, gv);
                 nrm = max(nrm, abs_bits(gv));
             }
             if (MODE & JAC) {
@@ -450,8 +437,8 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 const double gv = 0.0 + (v_i - gc());
                 const double gt = 0.0 + (th_i - gd());
                 if (MODE & RES) {
-                    gw.row(row_v, gv);
-                    gw.row(row_t, gt);
+                    st_out(A.g + ln + row_v * S, gv);
+                    st_out(A.g + ln + row_t * S, gt);
                 }
                 nrm = max(nrm, max(abs_bits(gv), abs_bits(gt)));
             }
@@ -490,7 +477,8 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
     }
 
     if (MODE & RES) {
-        gw.pq(i, N, acc_p, acc_q);
+        st_out(A.g + ln + i * S, acc_p);
+        st_out(A.g + ln + (N + i) * S, acc_q);
     }
     nrm = max(nrm, max(abs_bits(acc_p), abs_bits(acc_q)));
     if (MODE & JAC) {
@@ -512,8 +500,7 @@ __device__ __forceinline__ unsigned long long eval_bus(const DevicePlan& d, cons
                                                        const int32_t ln, const int32_t out_l) {
     GlobalSrc<S> src{d, A, A.y + ln, i, ln};
     return eval_bus_src<MODE, S>(d, tab, i, src, A, ln, out_l,
-                                 GlobalJ<S>{A.j ? A.j + ln : nullptr}, true,
-                                 GlobalG<S>{A.g ? A.g + ln : nullptr});
+                                 GlobalJ<S>{A.j ? A.j + ln : nullptr});
 }
 
 // Batched, persistent: gridDim.x CTAs (a few per SM) stride over work items
@@ -919,8 +906,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
                                 sbu + WS_ROWS * WS_ROW_BYTES, cnt.x, cnt.y};
             nrm = max(nrm, eval_bus_src<MODE, PF_LANES>(
                                d, tab, cnt.z, src, A, lane, out_l,
-                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk,
-                               GlobalG<PF_LANES>{A.g ? A.g + lane : nullptr}));
+                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk));
         }
         __syncwarp();         // slot reads done before it is refilled
     };
@@ -1352,8 +1338,7 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         SG_STAMP(4);
         if (own)   // phase B
             nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1,
-                                        StagedJ{jpb, jqb, jv, c1.x, c1.y, c1.z, c1.w}, true,
-                                        GlobalG<1>{g});
+                                        StagedJ{jpb, jqb, jv, c1.x, c1.y, c1.z, c1.w});
         if (MODE & (JAC | NORM)) __syncthreads();
         SG_STAMP(5);
         if (MODE & JAC) {   // staged rows out: one TMA bulk copy per range
