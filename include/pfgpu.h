@@ -31,6 +31,7 @@
 #ifndef PFGPU_H
 #define PFGPU_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -230,6 +231,13 @@ PF_API int pf_lu_residual(int32_t K, int32_t n, int32_t nnz, const int32_t* csr_
 
 /* Number of kernels this library has launched (process-wide counter). */
 PF_API int64_t pf_launch_count(void);
+
+/* Page-lock (and release) a caller-owned host range, so host-buffer calls
+ * on it move data by DMA at full PCIe rate (the workspaces register the
+ * state vector they are bound to).  Registering an already registered range
+ * and unregistering an unregistered one are no-ops. */
+PF_API int pf_host_register(void* ptr, size_t bytes);
+PF_API int pf_host_unregister(void* ptr);
 
 /* Number of device allocations this library has made (process-wide counter):
  * plan creation and the first host-buffer call per plan allocate; evaluations

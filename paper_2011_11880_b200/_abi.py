@@ -119,6 +119,8 @@ _SIGS = {
                                  _VP]),
     "pf_launch_count": (C.c_int64, []),
     "pf_alloc_count": (C.c_int64, []),
+    "pf_host_register": (C.c_int, [_VP, C.c_size_t]),
+    "pf_host_unregister": (C.c_int, [_VP]),
 }
 
 EXPORTED = tuple(_SIGS)

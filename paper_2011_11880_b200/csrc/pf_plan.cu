@@ -857,6 +857,28 @@ int64_t pf_launch_count(void) { return pf::g_launches.load(); }
 
 int64_t pf_alloc_count(void) { return pf::g_allocs.load(); }
 
+int pf_host_register(void* ptr, size_t bytes) {
+    if (!ptr || !bytes) return pf::invalid("NULL or empty host range");
+    const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();   // clear the sticky-free error state
+        return PF_OK;
+    }
+    PF_CUDA(e);
+    return PF_OK;
+}
+
+int pf_host_unregister(void* ptr) {
+    if (!ptr) return pf::invalid("NULL host pointer");
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e == cudaErrorHostMemoryNotRegistered) {
+        cudaGetLastError();
+        return PF_OK;
+    }
+    PF_CUDA(e);
+    return PF_OK;
+}
+
 int pf_plan_create(const pf_topology* topo, pf_plan** out) {
     if (!out) return pf::invalid("out is NULL");
     *out = nullptr;

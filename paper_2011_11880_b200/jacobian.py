@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 import scipy.sparse as sp
 
-from .plan import Plan, pinned_zeros
+from .plan import HostPin, Plan, pinned_zeros
 from .residual import ResidualWorkspace, evaluate_residual
 
 
@@ -46,6 +46,7 @@ class JacobianWorkspace:
         self.csc_perm = perm
         self._bound = None
         self._fresh_for = None   # id(y) whose J the paired residual run left in csc
+        self._pin = HostPin()
         if residual_ws is not None:
             residual_ws._paired = self
 
@@ -60,6 +61,8 @@ class JacobianWorkspace:
         if y.shape != (self.plan.n_var,):
             raise ValueError(f"state vector has shape {y.shape}, expected ({self.plan.n_var},)")
         self._bound = key
+        if isinstance(y, np.ndarray) and y.dtype == np.float64:
+            self._pin.hold(y)
 
     def run(self, y, cfg=None) -> sp.csc_matrix:
         self.bind(y, cfg)

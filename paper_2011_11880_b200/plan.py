@@ -37,15 +37,49 @@ def _stream_ptr(stream, device=None) -> int:
 def _on_device(fn):
     """Run a Plan method with the plan's device current: kernels launch, and
     plan-owned staging is allocated, in the plan's context whatever device
-    the caller has current."""
+    the caller has current (switched only when it differs)."""
     import functools
 
     @functools.wraps(fn)
     def wrapped(self, *a, **k):
-        with _torch().cuda.device(self.device):
+        torch = _torch()
+        if torch.cuda.current_device() == self.device.index:
+            return fn(self, *a, **k)
+        with torch.cuda.device(self.device):
             return fn(self, *a, **k)
 
     return wrapped
+
+
+class HostPin:
+    """Page-locks one caller-owned host array at a time (pf_host_register)
+    and keeps a reference to it until released, so the pages stay valid
+    while registered.  The workspaces pin the state vector they are bound to:
+    pflow's Newton loop keeps one y for the whole solve (newton.py:69), so
+    every upload after the first runs at full PCIe rate."""
+
+    def __init__(self):
+        self._arr = None
+
+    def hold(self, a) -> None:
+        if a is self._arr:
+            return
+        self.release()
+        if (isinstance(a, np.ndarray) and a.flags.c_contiguous and a.nbytes
+                and _torch().cuda.is_available()):
+            check(lib().pf_host_register(a.ctypes.data, a.nbytes))
+            self._arr = a
+
+    def release(self) -> None:
+        if self._arr is not None:
+            a, self._arr = self._arr, None
+            check(lib().pf_host_unregister(a.ctypes.data))
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
 
 
 def _host(a, n: int, name: str, dtype=np.float64):

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .plan import Plan, pinned_zeros
+from .plan import HostPin, Plan, pinned_zeros
 
 
 class ResidualWorkspace:
@@ -30,6 +30,7 @@ class ResidualWorkspace:
         self._bound = None
         self._out = None
         self._paired = None   # a JacobianWorkspace fused with this one (jacobian.py)
+        self._pin = HostPin()  # page-locks the bound state vector
 
     def bind(self, y, out, cfg=None):
         """Validate and remember the output buffer (pflow/residual.py:129-144)."""
@@ -46,6 +47,8 @@ class ResidualWorkspace:
             raise ValueError("residual vector must be contiguous float64")
         self._out = out
         self._bound = key
+        if isinstance(y, np.ndarray) and y.dtype == np.float64:
+            self._pin.hold(y)   # later uploads of y by DMA (residual.py:137-140 rebinds by id)
         return out
 
     def run(self, y, cfg=None):
