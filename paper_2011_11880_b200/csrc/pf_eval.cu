@@ -18,10 +18,13 @@
 // Batched mode maps the 32 lanes of a warp to 32 scenarios of the same bus:
 // topology loads are warp-uniform broadcasts and every state load / output
 // store is one fully coalesced 256-byte transaction (PF_LANES-blocked layout).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "pf_internal.cuh"
@@ -617,6 +620,22 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+// L2 policy of the plan reads that every scenario block repeats (packets,
+// stage records): evict-last when the plan keeps them (DevicePlan::ws_keep).
+// Rows of the scenario states get no hint: evict-last on them measured
+// slower (config 3 0.572 -> 0.589 with the packets kept, also at fractions
+// 0.5 and 0.25; config 4 -1 to -2 %).
+__device__ __forceinline__ uint64_t plan_policy(int32_t keep) {
+    uint64_t p;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void cp_async16_pol(uint32_t dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst),
+                 "l"(src), "l"(pol)
+                 : "memory");
+}
 constexpr int WS_ROW_BYTES = PF_LANES * 8;
 constexpr int WS_SLOT_BYTES = WS_ROWS * WS_ROW_BYTES + 32 * 16;   // rows + packet
 
@@ -714,6 +733,8 @@ struct StagedSrc : GlobalSrc<PF_LANES> {
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 0;" ::: "memory");
+        // the slot is refilled by TMA (async proxy) two steps later
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
 };
 
@@ -733,11 +754,17 @@ __device__ __forceinline__ void cp_async_wait() {
 // group per item.
 __device__ __forceinline__ void stage_item(const uint32_t sb, const int32_t rw,
                                            const int4* __restrict__ pkt,
-                                           const double* const* base, const int lane) {
+                                           const double* const* base, const int32_t keep,
+                                           const int lane) {
     const int32_t off = __shfl_sync(0xffffffffu, rw, 14);
     const int32_t meta = __shfl_sync(0xffffffffu, rw, 15);
     const int32_t units = meta & 0xffff, rows = meta >> 16;
-    if (lane < units) cp_async16(sb + WS_ROWS * WS_ROW_BYTES + lane * 16, pkt + off + lane);
+    if (lane < units) {
+        if (keep)
+            cp_async16_pol(sb + WS_ROWS * WS_ROW_BYTES + lane * 16, pkt + off + lane, plan_policy(1));
+        else
+            cp_async16(sb + WS_ROWS * WS_ROW_BYTES + lane * 16, pkt + off + lane);
+    }
     const double* src = nullptr;
     if (lane < rows && rw >= 0) {
         const double* bp = base[(uint32_t)rw >> 29];
@@ -753,18 +780,128 @@ __device__ __forceinline__ void stage_item(const uint32_t sb, const int32_t rw,
     cp_async_commit();
 }
 
+// ---- TMA staging (Blackwell tile::gather4) --------------------------------
+//
+// The same slot contents, moved by the tensor-memory accelerator instead of
+// per-lane cp.async: the scenario rows are rows of one 2-D tensor map
+// [rows x 32 doubles] whose base is the lowest of the launch's y / pq_p /
+// pq_q / pv_p arrays (every array sits a whole number of 256-byte rows above
+// it; launch_staged_kernel checks), so any four rows of the item, from any of
+// the arrays, are one gather4.  Lane 0 issues the packet as one bulk copy
+// and the rows as <= 3 gathers, all completing on the slot's mbarrier; rows
+// 12 and 13 (buses with many staged incidences) go by cp.async, since a
+// fourth gather would write past the rows into the packet.
+// Opt-in (PF_STAGING=tma), not the default: it executes 4.7 % fewer
+// instructions (config 3, ncu: 433 M against 454 M per launch) but measured
+// slower on B200 -- config 3 0.581 against 0.574 ms, config 4 0.550 against
+// 0.537 (profiles/r02_experiments.md): lane 0 issues every gather (the UTMALDG
+// operands must be moved to uniform registers one item at a time) while the
+// warp waits, and the kernel is not bound by the staging instructions.
+__device__ __forceinline__ void mbar_init(uint32_t m) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t m) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(m) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "PF_MBW:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra PF_MBW;\n}" ::"r"(m),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t m, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(m), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void gather4(uint32_t dst, const CUtensorMap* tm, uint32_t m,
+                                        int4 r) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(tm), "r"(m), "r"(0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w)
+        : "memory");
+}
+constexpr int WS_GATHER_ROWS = 12;   // rows moved by gather4 (3 x 4); the rest by cp.async
+
+// Issue the copies of one item into the slot at sb (mbarrier mb).  rw as in
+// stage_item; rb: this warp's row coordinate of entry 0 of each array of the
+// staged block (-1: array not passed); crd: the warp's 12-entry coordinate
+// scratch.  Rows of arrays not passed (the kernel reads plan constants for
+// them) and the padding of the last gather repeat row 0 (theta_i).
+__device__ __forceinline__ void stage_item_tma(const uint32_t sb, const uint32_t mb,
+                                               const int32_t rw, const int4* __restrict__ pkt,
+                                               const int32_t* rb, int32_t* crd,
+                                               const CUtensorMap* tm,
+                                               const double* const* tm_base,
+                                               const int32_t keep, const int lane) {
+    const int32_t off = __shfl_sync(0xffffffffu, rw, 14);
+    const int32_t meta = __shfl_sync(0xffffffffu, rw, 15);
+    const int32_t units = meta & 0xffff, rows = meta >> 16;
+    int32_t c = -1;
+    if (lane < rows && rw >= 0) {
+        const int32_t b = rb[(uint32_t)rw >> 29];
+        if (b >= 0) c = b + (rw & 0x1fffffff);
+    }
+    const int32_t c0 = __shfl_sync(0xffffffffu, c, 0);
+    if (c < 0) c = c0;
+    if (lane < WS_GATHER_ROWS) crd[lane] = c;
+    __syncwarp();
+    if (lane == 0) {
+        const int32_t ng = (min(rows, WS_GATHER_ROWS) + 3) >> 2;
+        mbar_expect_tx(mb, (uint32_t)(ng * 4 * WS_ROW_BYTES + units * 16));
+        bulk_g2s(sb + WS_ROWS * WS_ROW_BYTES, pkt + off, (uint32_t)(units * 16), mb,
+                 plan_policy(keep));
+        const uint32_t ca = smem_u32(crd);
+        for (int32_t q = 0; q < ng; ++q)
+            gather4(sb + q * 4 * WS_ROW_BYTES, tm, mb, lds_v4s32(ca + 16 * q));
+    }
+    if (rows > WS_GATHER_ROWS) {   // rows 12, 13: lanes 0-15 and 16-31
+        const int32_t r = WS_GATHER_ROWS + (lane >> 4);
+        const int32_t cr = __shfl_sync(0xffffffffu, c, r);
+        if (r < rows)
+            cp_async16(sb + r * WS_ROW_BYTES + (lane & 15) * 16,
+                       *tm_base + (int64_t)cr * PF_LANES + (lane & 15) * 2);
+    }
+    cp_async_commit();
+}
+
 // Each warp stages its own next item (no producer warp, no cross-warp
 // coupling): at the start of item k it issues item k+1's copies into its
 // other slot and loads item k+2's stage record, then waits for item k's
 // copies (issued one item earlier) and evaluates from shared memory.
-template <int MODE, int W, int MINB, bool DYN>
+// TMA = true: the slots are filled by stage_item_tma (tensor map tm over the
+// rows from tm_base; rb0: row coordinate of entry 0 of block 0 of y, pq_p,
+// pq_q, pv_p, -1 for an array not passed), false: by per-lane cp.async.
+template <int MODE, int W, int MINB, bool DYN, bool TMA>
 __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     const DevicePlan d, const int32_t K, const int32_t n_groups, const int32_t n_items,
     const double* __restrict__ y, const double* __restrict__ pq_p,
     const double* __restrict__ pq_q, const double* __restrict__ pv_p,
     const int32_t* __restrict__ outage, double* __restrict__ g, double* __restrict__ jv,
-    unsigned long long* __restrict__ norms, const uint32_t fd_m, const uint32_t fd_l) {
+    unsigned long long* __restrict__ norms, const uint32_t fd_m, const uint32_t fd_l,
+    const __grid_constant__ CUtensorMap tm, const double* __restrict__ tm_base, const int4 rb0) {
     extern __shared__ __align__(128) unsigned char ws_smem[];
+    __shared__ __align__(8) unsigned long long s_mb[W][2];   // TMA: one mbarrier per slot
+    __shared__ int32_t s_rb[W][4];                           // TMA: rb0 of the staged block
+    __shared__ __align__(16) int32_t s_crd[W][WS_GATHER_ROWS];
+    __shared__ const double* s_tmb;                          // TMA: tm_base
+    if (TMA && threadIdx.x == 0) s_tmb = tm_base;
+    if (TMA && (threadIdx.x & 31) == 0) {
+        mbar_init(smem_u32(&s_mb[threadIdx.x >> 5][0]));
+        mbar_init(smem_u32(&s_mb[threadIdx.x >> 5][1]));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __shared__ double s_tab[PF_TRIG_N * 4];
     __shared__ Scen<PF_LANES> As[W];   // per-warp block base pointers
     __shared__ int32_t s_ctr;          // dynamic mode: next slot claim of this CTA
@@ -814,8 +951,14 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         const int32_t it = item_of(x);
         const int32_t slot = (it - blk_of(it) * n_groups) * W + sub_of(x);
         if (slot >= d.N) return -1;
-        return __ldg(reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
-                     ((lane + 2) & 15));
+        const int32_t* rp = reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
+                            ((lane + 2) & 15);
+        if (!d.ws_keep) return __ldg(rp);
+        int32_t v;
+        asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;"
+                     : "=r"(v)
+                     : "l"(rp), "l"(plan_policy(1)));
+        return v;
     };
     // base pointers (y, pq_p, pq_q, pv_p) of the block being staged, per
     // warp in shared memory, refreshed when the staged block changes
@@ -823,22 +966,34 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     __shared__ int32_t s_sblk[W];
     if (lane == 0) s_sblk[warp] = -1;
     __syncwarp();
-    auto issue = [&](int32_t x, int32_t rw, uint32_t sb) {
+    auto issue = [&](int32_t x, int32_t rw, int s) {
+        const uint32_t sb = slots_u32 + s * WS_SLOT_BYTES;
+        const uint32_t mb = smem_u32(&s_mb[warp][s]);
         if (live(x) && __shfl_sync(0xffffffffu, rw, 14) >= 0) {
             const int32_t bb = blk_of(item_of(x));
             if (bb != s_sblk[warp]) {
                 __syncwarp();
                 if (lane == 0) s_sblk[warp] = bb;
                 if (lane < 4) {
-                    const double* a = lane == 0 ? y : lane == 1 ? pq_p : lane == 2 ? pq_q : pv_p;
                     const int64_t n = lane == 0 ? d.n_var : lane == 3 ? d.G : d.P;
-                    s_base[warp][lane] = a ? a + (int64_t)bb * n * PF_LANES : nullptr;
+                    if constexpr (TMA) {
+                        const int32_t r = lane == 0 ? rb0.x : lane == 1 ? rb0.y : lane == 2 ? rb0.z : rb0.w;
+                        s_rb[warp][lane] = r >= 0 ? r + (int32_t)(bb * n) : -1;
+                    } else {
+                        const double* a = lane == 0 ? y : lane == 1 ? pq_p : lane == 2 ? pq_q : pv_p;
+                        s_base[warp][lane] = a ? a + (int64_t)bb * n * PF_LANES : nullptr;
+                    }
                 }
                 __syncwarp();
             }
-            stage_item(sb, rw, d.ws_pkt, s_base[warp], lane);
+            if constexpr (TMA)
+                stage_item_tma(sb, mb, rw, d.ws_pkt, s_rb[warp], s_crd[warp], &tm, &s_tmb,
+                               d.ws_keep, lane);
+            else
+                stage_item(sb, rw, d.ws_pkt, s_base[warp], d.ws_keep, lane);
         } else {
-            cp_async_commit();   // keep one group per step
+            if (TMA && lane == 0) mbar_arrive(mb);   // complete the slot's phase
+            cp_async_commit();                       // keep one group per step
         }
     };
 
@@ -892,6 +1047,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     };
     // evaluate step k (slot `slot` of block `blk`) from its staging slot
     auto evaluate = [&](int32_t k, int32_t blk, int32_t slot) {
+        if constexpr (TMA) mbar_wait(smem_u32(&s_mb[warp][k & 1]), (uint32_t)(k >> 1) & 1);
         cp_async_wait<1>();   // this step's group has landed (own lanes)
         __syncwarp();         // ... and every lane's
         unsigned char* sb = slots + (k & 1) * WS_SLOT_BYTES;
@@ -920,7 +1076,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         };
         {   // prologue: step 0's copies in flight, step 1's record in a register
             const int32_t q0 = claim();
-            issue(q0, rec_word(q0), slots_u32);
+            issue(q0, rec_word(q0), 0);
             const int32_t q1 = claim();
             if (lane == 0) {
                 s_q[warp][0] = q0;
@@ -940,57 +1096,13 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             // iteration); load step k+2's record
             const int32_t q2 = claim();
             if (lane == 0) s_q[warp][(k + 2) & 3] = q2;
-            issue(s_q[warp][(k + 1) & 3], rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
+            issue(s_q[warp][(k + 1) & 3], rw_next, (k + 1) & 1);
             rw_next = rec_word(q2);
             evaluate(k, blk, (item - blk * n_groups) * W + q % W);
         }
     } else {
-#ifdef PF_X_CONTIG
-        // CTA-contiguous groups: in every scenario block CTA c takes the
-        // groups [lo, hi) of an even split, so its J and g rows form one long
-        // ascending stream per block instead of W-bus windows G groups apart.
-        const int32_t lo = (int32_t)(((int64_t)n_groups * blockIdx.x) / stride);
-        const int32_t nc = (int32_t)(((int64_t)n_groups * (blockIdx.x + 1)) / stride) - lo;
-        const int32_t nblk = n_groups ? n_items / n_groups : 0;
-        const int32_t steps = nc * nblk;
-        auto cword = [&](int32_t k) -> int32_t {
-            if (k >= steps) return -1;
-            const int32_t b = k / nc;
-            const int32_t slot = (lo + (k - b * nc)) * W + warp;
-            if (slot >= d.N) return -1;
-            return __ldg(reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
-                         ((lane + 2) & 15));
-        };
-        auto cissue = [&](int32_t k, int32_t rw, uint32_t sb) {
-            if (k < steps && __shfl_sync(0xffffffffu, rw, 14) >= 0) {
-                const int32_t bb = k / nc;
-                if (bb != s_sblk[warp]) {
-                    __syncwarp();
-                    if (lane == 0) s_sblk[warp] = bb;
-                    if (lane < 4) {
-                        const double* a = lane == 0 ? y : lane == 1 ? pq_p : lane == 2 ? pq_q : pv_p;
-                        const int64_t n = lane == 0 ? d.n_var : lane == 3 ? d.G : d.P;
-                        s_base[warp][lane] = a ? a + (int64_t)bb * n * PF_LANES : nullptr;
-                    }
-                    __syncwarp();
-                }
-                stage_item(sb, rw, d.ws_pkt, s_base[warp], lane);
-            } else {
-                cp_async_commit();
-            }
-        };
-        cissue(0, cword(0), slots_u32);
-        int32_t rw_next = cword(1);
-        for (int32_t k = 0; k < steps; ++k) {
-            const int32_t blk = k / nc;
-            if (blk != cur) enter_block(blk);
-            cissue(k + 1, rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
-            rw_next = cword(k + 2);
-            evaluate(k, blk, (lo + (k - blk * nc)) * W + warp);
-        }
-#else
         // prologue: item 0's copies in flight, item 1's record in a register
-        issue(blockIdx.x, rec_word(blockIdx.x), slots_u32);
+        issue(blockIdx.x, rec_word(blockIdx.x), 0);
         int32_t rw_next = rec_word(blockIdx.x + stride);
         int32_t k = 0;
         for (int32_t item = blockIdx.x; item < n_items; item += stride, ++k) {
@@ -999,11 +1111,10 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             // next item's copies into the other slot (its previous contents,
             // item k-1, were consumed in the previous iteration), then the
             // record of the item after it
-            issue(item + stride, rw_next, slots_u32 + ((k + 1) & 1) * WS_SLOT_BYTES);
+            issue(item + stride, rw_next, (k + 1) & 1);
             rw_next = rec_word(item + 2 * stride);
             evaluate(k, blk, (item - blk * n_groups) * W + warp);
         }
-#endif
     }
     cp_async_wait<0>();
     if (cur >= 0) flush(cur);
@@ -1700,12 +1811,78 @@ static cudaError_t launch_batched_mode(const DevicePlan& d, int32_t K, const dou
 // Staged kernel shape (pf_internal.cuh WS_W, WS_MINB): two 4 KB slots per
 // warp in dynamic shared memory.
 constexpr size_t WS_SMEM = (size_t)WS_W * 2 * WS_SLOT_BYTES;
-template <int MODE, bool DYN>
+
+// The row tensor map of a launch (stage_item_tma): base = the lowest of the
+// arrays passed, every array a whole number of 256-byte rows above it, all
+// rows addressable with int32 coordinates.  Encoded on the host per launch
+// (a pure host call, ~1 us); false when the arrays do not qualify or the
+// driver lacks the entry point, and the launch uses cp.async staging.
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+static bool use_tma_staging() {
+    static const bool v = [] {
+        const char* e = getenv("PF_STAGING");
+        return e && e[0] == 't';   // "tma": gather4 staging (opt-in, see k_eval_staged)
+    }();
+    return v;
+}
+
+static bool row_tensor_map(const DevicePlan& d, int32_t K, const double* y, const double* pq_p,
+                           const double* pq_q, const double* pv_p, CUtensorMap* tm,
+                           const double** base, int4* rb0) {
+    if (!use_tma_staging()) return false;
+    const auto enc = tma_encoder();
+    if (!enc || !y) return false;
+    const int64_t nblk = (K + PF_LANES - 1) / PF_LANES;
+    const double* arr[4] = {y, pq_p, pq_q, pv_p};
+    const int64_t len[4] = {d.n_var, d.P, d.P, d.G};
+    uintptr_t lo = UINTPTR_MAX;
+    for (int a = 0; a < 4; ++a)
+        if (arr[a]) lo = std::min(lo, reinterpret_cast<uintptr_t>(arr[a]));
+    if (lo % 16) return false;
+    int32_t r[4];
+    int64_t rows = 1;
+    for (int a = 0; a < 4; ++a) {
+        r[a] = -1;
+        if (!arr[a]) continue;
+        const uintptr_t off = reinterpret_cast<uintptr_t>(arr[a]) - lo;
+        if (off % WS_ROW_BYTES) return false;
+        const int64_t r0 = (int64_t)(off / WS_ROW_BYTES), end = r0 + nblk * len[a];
+        if (end >= (1ll << 31)) return false;
+        r[a] = (int32_t)r0;
+        rows = std::max(rows, end);
+    }
+    cuuint64_t gdim[2] = {(cuuint64_t)PF_LANES, (cuuint64_t)rows};
+    cuuint64_t gstr[1] = {(cuuint64_t)WS_ROW_BYTES};
+    cuuint32_t box[2] = {(cuuint32_t)PF_LANES, 1};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, reinterpret_cast<void*>(lo), gdim, gstr, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    *base = reinterpret_cast<const double*>(lo);
+    *rb0 = make_int4(r[0], r[1], r[2], r[3]);
+    return true;
+}
+
+template <int MODE, bool DYN, bool TMA>
 static cudaError_t launch_staged_kernel(const DevicePlan& d, int32_t K, const double* y,
                                       const double* pq_p, const double* pq_q,
                                       const double* pv_p, const int32_t* outage, double* g,
-                                      double* j, double* norms, cudaStream_t st) {
-    auto kern = k_eval_staged<MODE, WS_W, WS_MINB, DYN>;
+                                      double* j, double* norms, const CUtensorMap& tm,
+                                      const double* tm_base, int4 rb0, cudaStream_t st) {
+    auto kern = k_eval_staged<MODE, WS_W, WS_MINB, DYN, TMA>;
     static DevLaunchCfg tab[PF_MAX_DEVICES];
     const DevLaunchCfg* dc = nullptr;
     cudaError_t e = device_cfg(tab, kern, 32 * WS_W, WS_SMEM, &dc);
@@ -1725,7 +1902,7 @@ static cudaError_t launch_staged_kernel(const DevicePlan& d, int32_t K, const do
     kern<<<grid, 32 * WS_W, WS_SMEM, st>>>(d, K, n_groups, n_items, y, pq_p, pq_q, pv_p,
                                            outage, g, j,
                                            reinterpret_cast<unsigned long long*>(norms), fd_m,
-                                           fd_l);
+                                           fd_l, tm, tm_base, rb0);
     return cudaSuccess;
 }
 
@@ -1744,9 +1921,16 @@ static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const doub
         return !e ? -1 : (e[0] == 'd' ? 1 : (e[0] == 's' ? 0 : -1));
     }();
     const bool dyn = forced >= 0 ? forced == 1 : (int64_t)d.n_hubs * 200 >= d.N;
-    if (dyn)
-        return launch_staged_kernel<MODE, true>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st);
-    return launch_staged_kernel<MODE, false>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, st);
+    CUtensorMap tm;
+    std::memset(&tm, 0, sizeof tm);
+    const double* base = nullptr;
+    int4 rb0 = make_int4(-1, -1, -1, -1);
+    const bool tma = row_tensor_map(d, K, y, pq_p, pq_q, pv_p, &tm, &base, &rb0);
+#define PF_K(D, T) \
+    launch_staged_kernel<MODE, D, T>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, tm, base, rb0, st)
+    if (dyn) return tma ? PF_K(true, true) : PF_K(true, false);
+    return tma ? PF_K(false, true) : PF_K(false, false);
+#undef PF_K
 }
 
 static bool use_staged() {

@@ -104,6 +104,8 @@ struct DevicePlan {
     int32_t n_hubs;           // buses with degree >= HUB_DEG
     const int4* ws_pkt;       // staged-kernel packets (see WS_ROWS above)
     const int4* ws_rec;       // [N * WS_REC_WORDS / 4] stage records in processing order
+    int32_t ws_keep;          // 1: packets and records are read with an L2 evict-last
+                              // policy (they fit in L2 beside one block's states)
     const int32_t* dev_ptr;   // [N+1]
     const int4* dev_list;     // [n_dev] {type, index, jpos_a, jpos_b}
     // device parameters (base values; scenarios may override P/Q)

@@ -832,6 +832,14 @@ int build(const pf_topology* t, pf_plan** out) {
                               cudaMemcpyHostToDevice));
         d.ws_pkt = dpkt;
         d.ws_rec = drec;
+        // Packets and records are re-read by every 32-scenario block; they stay
+        // in L2 across blocks (evict-last) when they and one block's state rows
+        // take at most half of it.  B200, ms per launch: config 3 (19 MB +
+        // 37 MB) 0.595 -> 0.572; config 4 (51 MB + 110 MB, not kept) would
+        // lose 0.533 -> 0.537.
+        const int64_t keep = (int64_t)pkt.size() * 16 + (int64_t)N * WS_REC_WORDS * 4 +
+                             (int64_t)d.n_var * PF_LANES * 8;
+        d.ws_keep = keep <= (64ll << 20) ? 1 : 0;
     }
     count_launch(12);
     *out = P;

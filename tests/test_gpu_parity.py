@@ -897,8 +897,9 @@ def test_device_batched_sparse_lu_vs_scipy():
 def test_previous_batched_kernel_still_matches(tmp_path):
     """PF_BATCHED_KERNEL=old selects the previous single-role batched kernel
     (kept for A/B timing, scripts/ab_env.sh), PF_SCHEDULE forces the staged
-    kernel's static or dynamic schedule; in fresh processes every variant
-    must give the same bits as the default."""
+    kernel's static or dynamic schedule, PF_STAGING=tma its TMA gather4
+    staging; in fresh processes every variant must give the same bits as the
+    default."""
     import subprocess
     import sys
 
@@ -925,16 +926,18 @@ np.savez(sys.argv[2], g=g.cpu().numpy(), j=j.cpu().numpy(), n=n.cpu().numpy())
     root = str(Path(__file__).resolve().parents[1])
     outs = {}
     runs = {"staged": {}, "old": {"PF_BATCHED_KERNEL": "old"},
-            "static": {"PF_SCHEDULE": "static"}, "dynamic": {"PF_SCHEDULE": "dynamic"}}
+            "static": {"PF_SCHEDULE": "static"}, "dynamic": {"PF_SCHEDULE": "dynamic"},
+            "tma_static": {"PF_STAGING": "tma", "PF_SCHEDULE": "static"},
+            "tma_dynamic": {"PF_STAGING": "tma", "PF_SCHEDULE": "dynamic"}}
     for kind, extra in runs.items():
         env = dict(os.environ)
-        env.pop("PF_BATCHED_KERNEL", None)
-        env.pop("PF_SCHEDULE", None)
+        for v in ("PF_BATCHED_KERNEL", "PF_SCHEDULE", "PF_STAGING"):
+            env.pop(v, None)
         env.update(extra)
         f = tmp_path / f"{kind}.npz"
         subprocess.run([sys.executable, "-c", code, root, str(f)], check=True, env=env)
         outs[kind] = np.load(f)
-    for kind in ("old", "static", "dynamic"):
+    for kind in runs:
         for k in ("g", "j", "n"):
             assert np.array_equal(outs["staged"][k], outs[kind][k]), (kind, k)
 
