@@ -18,6 +18,8 @@ from paper_2011_11880_b200._abi import lib  # noqa: E402
 from paper_2011_11880_b200.plan import Plan  # noqa: E402
 from paper_2011_11880_b200.system_model import build_system, random_state  # noqa: E402
 
+import os
+MODE = os.environ.get("MODE", "fjn")   # outputs: f (g), j (J), n (norm)
 NAMES = ["start", "pre-wait", "wait done", "y loaded", "phase A", "phase B", "norm", "end"]
 for cfg in [int(a) for a in sys.argv[1:]] or [0, 2]:
     s = build_system(synth.config_case(cfg, seed=cfg))
@@ -32,7 +34,8 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 2]:
     gr = torch.cuda.CUDAGraph()
     with torch.cuda.graph(gr, stream=st):
         for k in range(10):
-            plan.eval(ys[k], g, j, n)
+            plan.eval(ys[k], g if "f" in MODE else None, j if "j" in MODE else None,
+                      n if "n" in MODE else None)
     for _ in range(3):
         gr.replay()
     torch.cuda.synchronize()
@@ -41,7 +44,7 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 2]:
     tr = buf.astype(np.int64).reshape(4096, 8)[: plan.single_chunks]
     t0 = tr[:, 2].min()
     rel = (tr - t0) / 1000.0
-    print(f"config {cfg}: {len(tr)} CTAs (µs from the first wait return)")
+    print(f"[{MODE}] config {cfg}: {len(tr)} CTAs (µs from the first wait return)")
     for k, nm in enumerate(NAMES):
         c = rel[:, k]
         print(f"  {nm:10s} min {c.min():7.2f}  median {np.median(c):7.2f}  max {c.max():7.2f}")
