@@ -886,7 +886,7 @@ __device__ __forceinline__ void stage_item_tma(const uint32_t sb, const uint32_t
 // TMA = true: the slots are filled by stage_item_tma (tensor map tm over the
 // rows from tm_base; rb0: row coordinate of entry 0 of block 0 of y, pq_p,
 // pq_q, pv_p, -1 for an array not passed), false: by per-lane cp.async.
-template <int MODE, int W, int MINB, bool DYN, bool TMA>
+template <int MODE, int W, int MINB, bool DYN, bool TMA, bool KEEP>
 __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
     const DevicePlan d, const int32_t K, const int32_t n_groups, const int32_t n_items,
     const double* __restrict__ y, const double* __restrict__ pq_p,
@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
         if (slot >= d.N) return -1;
         const int32_t* rp = reinterpret_cast<const int32_t*>(d.ws_rec) + (int64_t)slot * WS_REC_WORDS +
                             ((lane + 2) & 15);
-        if (!d.ws_keep) return __ldg(rp);
+        if (!KEEP) return __ldg(rp);
         int32_t v;
         asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;"
                      : "=r"(v)
@@ -991,9 +991,9 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             }
             if constexpr (TMA)
                 stage_item_tma(sb, mb, rw, d.ws_pkt, s_rb[warp], s_crd[warp], &tm, &s_tmb,
-                               d.ws_keep, lane);
+                               KEEP, lane);
             else
-                stage_item(sb, rw, d.ws_pkt, s_base[warp], d.ws_keep, lane);
+                stage_item(sb, rw, d.ws_pkt, s_base[warp], KEEP, lane);
         } else {
             if (TMA && lane == 0) mbar_arrive(mb);   // complete the slot's phase
             cp_async_commit();                       // keep one group per step
@@ -1887,13 +1887,13 @@ static bool row_tensor_map(const DevicePlan& d, int32_t K, const double* y, cons
     return true;
 }
 
-template <int MODE, bool DYN, bool TMA>
+template <int MODE, bool DYN, bool TMA, bool KEEP>
 static cudaError_t launch_staged_kernel(const DevicePlan& d, int32_t K, const double* y,
                                       const double* pq_p, const double* pq_q,
                                       const double* pv_p, const int32_t* outage, double* g,
                                       double* j, double* norms, const CUtensorMap& tm,
                                       const double* tm_base, int4 rb0, cudaStream_t st) {
-    auto kern = k_eval_staged<MODE, WS_W, WS_MINB, DYN, TMA>;
+    auto kern = k_eval_staged<MODE, WS_W, WS_MINB, DYN, TMA, KEEP>;
     static DevLaunchCfg tab[PF_MAX_DEVICES];
     const DevLaunchCfg* dc = nullptr;
     cudaError_t e = device_cfg(tab, kern, 32 * WS_W, WS_SMEM, &dc);
@@ -1937,10 +1937,12 @@ static cudaError_t launch_staged_mode(const DevicePlan& d, int32_t K, const doub
     const double* base = nullptr;
     int4 rb0 = make_int4(-1, -1, -1, -1);
     const bool tma = row_tensor_map(d, K, y, pq_p, pq_q, pv_p, &tm, &base, &rb0);
-#define PF_K(D, T) \
-    launch_staged_kernel<MODE, D, T>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, tm, base, rb0, st)
-    if (dyn) return tma ? PF_K(true, true) : PF_K(true, false);
-    return tma ? PF_K(false, true) : PF_K(false, false);
+#define PF_K(D, T, KP) \
+    launch_staged_kernel<MODE, D, T, KP>(d, K, y, pq_p, pq_q, pv_p, outage, g, j, norms, tm, base, rb0, st)
+    // (the plan's L2 policy is a template parameter: no per-item branch)
+    if (tma) return dyn ? PF_K(true, true, false) : PF_K(false, true, false);
+    if (d.ws_keep) return dyn ? PF_K(true, false, true) : PF_K(false, false, true);
+    return dyn ? PF_K(true, false, false) : PF_K(false, false, false);
 #undef PF_K
 }
 
