@@ -62,6 +62,22 @@ def algorithmic_bytes(sys_, nnz: int, K: int) -> tuple[int, int, int]:
     return per_scen, static, per_scen * K + static
 
 
+def workload_config(workload: str, sys_, nnz: int) -> dict:
+    """The line's `config`: properties of the workload only, computed the same
+    way by both arms (so the driver sees one config); how an arm runs it
+    goes in the line's `run`."""
+    import numpy as np
+
+    K = WORKLOADS[workload][1]
+    _, _, by = algorithmic_bytes(sys_, nnz, K)
+    deg = np.bincount(np.concatenate([sys_.lines.bus_h, sys_.lines.bus_k]),
+                      minlength=sys_.n_bus)
+    return {"workload": workload_desc(workload), "n_var": int(sys_.n_var), "nnz": int(nnz),
+            "scenarios_total": K, "max_bus_degree": int(deg.max()) if deg.size else 0,
+            "l2": (f"inputs+outputs of the {K}-scenario step {by / 1e9:.2f} GB > 126 MB L2 "
+                   "(no flush needed)")}
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
@@ -191,7 +207,7 @@ def cpu_reference(sys_, K, seed, steps, warmup, threads, min_seconds=0.0):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     return {"value": K * len(times) / total, "ms_per_step": 1e3 * total / len(times),
-            "wf": wf, "steps": len(times), "threads": threads}
+            "wf": wf, "steps": len(times), "threads": threads, "nnz": int(o.nnz)}
 
 
 def run_reference(args):
@@ -208,9 +224,9 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(args.workload),
-                   "parallelism": f"{threads} host threads, one scenario per thread at a time "
-                                  "(CPU only; the N GPUs are unused)"},
+        "config": workload_config(args.workload, sys_, r["nnz"]),
+        "run": {"parallelism": f"{threads} host threads, one scenario per thread at a time "
+                               "(CPU only; the N GPUs are unused)"},
         "cpu_baseline": {"value": r["value"], "unit": "evals/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{r['steps']} steps x {K} scenarios, pflow wf{r['wf']} "
@@ -325,6 +341,7 @@ def batched_leg(args, workload: str, scaling: str, dev, rank: int, world: int,
             "workload": workload_desc(workload), "scenarios_total": K_total,
             "scenarios_per_gpu": K, "gpu_launches": launches, "clocks": clk,
             "n_var": plan.n_var, "nnz": plan.nnz, "max_bus_degree": plan.max_degree,
+            "config": workload_config(workload, sys_, plan.nnz),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_of(workload),
                          "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_launch,
@@ -454,14 +471,13 @@ def run_gpu(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {
-                "workload": head["workload"], "n_var": head["n_var"], "nnz": head["nnz"],
-                "scenarios_total": head["scenarios_total"],
+            "config": head["config"],
+            "run": {
                 "scenarios_per_gpu": head["scenarios_per_gpu"],
                 "parallelism": f"scenario-sharded x{world} ({scaling} scaling)"
                                + (", NCCL all-gather of norms overlapped with the next step"
                                   if world > 1 else ""),
-                "l2": head["l2"], "max_bus_degree": head["max_bus_degree"],
+                "l2": head["l2"],
             },
             "roofline": head["roofline"], "e2e": head["e2e"],
             "e2e_device_resident": head["e2e_device_resident"],
