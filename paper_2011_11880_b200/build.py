@@ -39,7 +39,8 @@ def source_hash() -> str:
                      ROOT / "include" / "pfgpu.h"]):
         h.update(p.name.encode())
         h.update(p.read_bytes())
-    h.update(repr((COMMON, UNITS)).encode())
+    # flags without the checkout's absolute path (the GPU box runs a copy elsewhere)
+    h.update(repr(([f.replace(str(ROOT), "<root>") for f in COMMON], UNITS)).encode())
     return h.hexdigest()[:16]
 
 
