@@ -215,33 +215,40 @@ __device__ __forceinline__ void inc_fold(const IncVals& v, double& acc_p, double
 // Jacobian writers.  GlobalJ stores straight to the value array (batched:
 // lane stride S); StagedJ (single grid) keeps the rows g_p, g_q of the CTA's
 // buses in shared memory and writes other rows (g_V, g_theta) through.
+// Writers take the row kind: p (row g_p[i] of the bus being evaluated), q
+// (row g_q[i]) or x (any other row: g_V, g_theta).
 template <int S>
 struct GlobalJ {
     double* __restrict__ jv;
     __device__ __forceinline__ void put(int32_t at, double v) const { st_out(jv + at * S, v); }
+    __device__ __forceinline__ void put_p(int32_t at, double v) const { put(at, v); }
+    __device__ __forceinline__ void put_q(int32_t at, double v) const { put(at, v); }
+    __device__ __forceinline__ void put_x(int32_t at, double v) const { put(at, v); }
     // reference assembly: acc = 0.0; acc += slot ... (kernels.py:277-282)
-    __device__ __forceinline__ void add(int32_t at, bool first, double v) const {
+    __device__ __forceinline__ void add_p(int32_t at, bool first, double v) const {
+        put_offdiag<S>(jv, at, first, v);
+    }
+    __device__ __forceinline__ void add_q(int32_t at, bool first, double v) const {
         put_offdiag<S>(jv, at, first, v);
     }
 };
 
+// The chunk's rows g_p[b0..b1) and g_q[b0..b1) are staged, so p / q
+// entries of its buses go to shared memory without a range test.
 struct StagedJ {
     double* jp;                   // staged rows g_p[b0..b1): jp[k] is jv[p0 + k]
     double* jq;                   // staged rows g_q[b0..b1): jq[k] is jv[q0 + k]
     double* __restrict__ jv;
-    int32_t p0, p1, q0, q1;
-    __device__ __forceinline__ double* loc(int32_t at) const {
-        if (at >= p0 && at < p1) return jp + (at - p0);
-        if (at >= q0 && at < q1) return jq + (at - q0);
-        return nullptr;
+    int32_t p0, q0;
+    __device__ __forceinline__ void put_p(int32_t at, double v) const { jp[at - p0] = v; }
+    __device__ __forceinline__ void put_q(int32_t at, double v) const { jq[at - q0] = v; }
+    __device__ __forceinline__ void put_x(int32_t at, double v) const { jv[at] = v; }
+    __device__ __forceinline__ void add_p(int32_t at, bool first, double v) const {
+        double* p = jp + (at - p0);
+        *p = first ? 0.0 + v : *p + v;
     }
-    __device__ __forceinline__ void put(int32_t at, double v) const {
-        double* p = loc(at);
-        if (p) *p = v;
-        else jv[at] = v;
-    }
-    __device__ __forceinline__ void add(int32_t at, bool first, double v) const {
-        double* p = loc(at);   // off-diagonals always lie in the staged rows
+    __device__ __forceinline__ void add_q(int32_t at, bool first, double v) const {
+        double* p = jq + (at - q0);
         *p = first ? 0.0 + v : *p + v;
     }
 };
@@ -255,15 +262,15 @@ __device__ __forceinline__ void inc_offdiag(const IncVals& v, const int4 m, cons
     // one (warp-uniform) branch per incidence: the common first-neighbour
     // stores, or the rare parallel-branch read-modify-writes
     if (first) {
-        jw.add(rp + pos, true, v.opt);
-        jw.add(rp + nb + pos, true, v.opv);
-        jw.add(rq + pos, true, v.oqt);
-        jw.add(rq + nb + pos, true, v.oqv);
+        jw.add_p(rp + pos, true, v.opt);
+        jw.add_p(rp + nb + pos, true, v.opv);
+        jw.add_q(rq + pos, true, v.oqt);
+        jw.add_q(rq + nb + pos, true, v.oqv);
     } else {
-        jw.add(rp + pos, false, v.opt);
-        jw.add(rp + nb + pos, false, v.opv);
-        jw.add(rq + pos, false, v.oqt);
-        jw.add(rq + nb + pos, false, v.oqv);
+        jw.add_p(rp + pos, false, v.opt);
+        jw.add_p(rp + nb + pos, false, v.opv);
+        jw.add_q(rq + pos, false, v.oqt);
+        jw.add_q(rq + nb + pos, false, v.oqv);
     }
 }
 
@@ -429,8 +436,8 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 nrm = max(nrm, abs_bits(gv));
             }
             if (MODE & JAC) {
-                jw.put(dv.z, 1.0);   // (g_q[i], Q_g)   kernels.py:244-247
-                jw.put(dv.w, 1.0);   // (g_V, V_i)
+                jw.put_q(dv.z, 1.0);   // (g_q[i], Q_g)   kernels.py:244-247
+                jw.put_x(dv.w, 1.0);   // (g_V, V_i)
             }
         } else if (dv.x == DEV_SLACK) {
             const int32_t q = d.G + k;    // sl_qg, sl_ps are aranges (plan-checked)
@@ -449,10 +456,10 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                 nrm = max(nrm, max(abs_bits(gv), abs_bits(gt)));
             }
             if (MODE & JAC) {
-                jw.put(dv.z, 1.0);                                   // (g_p, P_s)
-                jw.put(dv.w, 1.0);                                   // (g_q, Q_g)
-                jw.put(__ldg(d.gen_row_pos + q), 1.0);               // (g_V, V)
-                jw.put(__ldg(d.gen_row_pos + d.n_gen + ps), 1.0);    // (g_theta, theta)
+                jw.put_p(dv.z, 1.0);                                   // (g_p, P_s)
+                jw.put_q(dv.w, 1.0);                                   // (g_q, Q_g)
+                jw.put_x(__ldg(d.gen_row_pos + q), 1.0);               // (g_V, V)
+                jw.put_x(__ldg(d.gen_row_pos + d.n_gen + ps), 1.0);    // (g_theta, theta)
             }
         } else {  // DEV_SHUNT (kernels.py:236-241, 258-262)
             const double gsh = gc(), bsh = gd();
@@ -489,12 +496,12 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
     nrm = max(nrm, max(abs_bits(acc_p), abs_bits(acc_q)));
     if (MODE & JAC) {
         if (nb > 0) {
-            jw.put(rp + pos_i, d_pt);
-            jw.put(rq + pos_i, d_qt);
+            jw.put_p(rp + pos_i, d_pt);
+            jw.put_q(rq + pos_i, d_qt);
         }
         if (vdiag) {
-            jw.put(rp + nb + pos_i, d_pv);
-            jw.put(rq + nb + pos_i, d_qv);
+            jw.put_p(rp + nb + pos_i, d_pv);
+            jw.put_q(rq + nb + pos_i, d_qv);
         }
     }
     return nrm;
@@ -1451,7 +1458,7 @@ __global__ void __launch_bounds__(SG_THREADS, SG_MINB) k_eval_single(const Devic
         SG_STAMP(4);
         if (own)   // phase B
             nrm = eval_bus_src<MODE, 1>(d, tab, i, src, A, 0, -1,
-                                        StagedJ{jpb, jqb, jv, c1.x, c1.y, c1.z, c1.w});
+                                        StagedJ{jpb, jqb, jv, c1.x, c1.z});
         if (MODE & NORM) norm_post(nrm, red);
         if (MODE & (JAC | NORM)) __syncthreads();
         SG_STAMP(5);
