@@ -296,6 +296,18 @@ struct StagedPrefix<Src, decltype(void(Src::kStaged))> {
     static constexpr bool value = Src::kStaged;
 };
 
+// Sources holding a bus's first two devices in registers (the single-grid
+// source) set kRegDev: those two are evaluated without the generic device
+// loop's index selects.
+template <class Src, class = void>
+struct RegDevices {
+    static constexpr bool value = false;
+};
+template <class Src>
+struct RegDevices<Src, decltype(void(Src::kRegDev))> {
+    static constexpr bool value = Src::kRegDev;
+};
+
 // Staged sources that can reuse their slot for the incidences past the
 // staged prefix (chunks of the prefix's size) set kChunked.
 template <class Src, class = void>
@@ -481,6 +493,16 @@ __device__ __forceinline__ unsigned long long eval_bus_src(const DevicePlan& d, 
                      [&] { return src.sdev_c(u); }, [&] { return src.sdev_d(u); });
         }
         t0 += nv;
+    }
+    if constexpr (RegDevices<Src>::value) {
+        const int32_t nd = rng.w - rng.z;
+        if (nd > 0)
+            dev_step(src.dv0, [&] { return src.a0; }, [&] { return src.b0; },
+                     [&] { return src.c0; }, [&] { return src.d0; });
+        if (nd > 1)
+            dev_step(src.dv1, [&] { return src.a1; }, [&] { return src.b1; },
+                     [&] { return src.c1; }, [&] { return src.d1; });
+        t0 += min(nd, 2);
     }
     for (int32_t t = t0; t < rng.w; ++t) {
         const int32_t u = t - rng.z;
@@ -1149,6 +1171,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
 // before griddepcontrol.wait, the state and every output after it.
 struct SingleSrc : GlobalSrc<1> {
     static constexpr bool kSplit = true;
+    static constexpr bool kRegDev = true;
     const double* fold;                // [n_inc of chunk][6] {fp, fq, pt, pv, qt, qv}
     const double* dupv;                // [dup slots][4] {opt, opv, oqt, oqv}
     int32_t E0;
