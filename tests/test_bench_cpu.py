@@ -24,6 +24,15 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["metric"].startswith("f+J evals/s")
+    # the config holds workload properties only, computed as the GPU arm does
+    # (bench.workload_config); how this arm ran goes in "run"
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    sys_ = bench.build_case("config3")
+    assert d["config"] == bench.workload_config("config3", sys_, d["config"]["nnz"])
+    assert d["config"]["n_var"] == sys_.n_var and d["config"]["scenarios_total"] == 256
+    assert "parallelism" in d["run"]
 
 
 def test_reference_arm_other_ranks_exit_quietly():
