@@ -261,7 +261,7 @@ def batched_leg(args, workload: str, scaling: str, dev, rank: int, world: int,
     import torch
     import torch.distributed as dist
 
-    from paper_2011_11880_b200.batched import NormExchange, max_shard
+    from paper_2011_11880_b200.batched import NormExchange, check_same_pattern, max_shard
     from paper_2011_11880_b200.plan import Plan, launch_count
 
     K_total, lo, hi, seed, K_gen = rank_workload(workload, scaling, rank, world)
@@ -272,6 +272,8 @@ def batched_leg(args, workload: str, scaling: str, dev, rank: int, world: int,
     t1 = time.perf_counter()
     plan = Plan(sys_, device=dev)
     torch.cuda.synchronize(dev)
+    if world > 1:   # every rank built the same pattern
+        check_same_pattern(*plan.pattern_csr(), device=dev)
     setup_s = {"build_system_s": t1 - t0, "plan_create_s": time.perf_counter() - t1,
                "note": "synthetic case generation + build_system (host), then pf_plan_create: "
                        "upload, device symbolic pattern, staging records"}

@@ -166,6 +166,38 @@ class NormExchange:
                           enumerate(shard(K_total, r, self.world) for r in range(self.world))])
 
 
+def pattern_digest(indptr, indices) -> int:
+    """63-bit digest of a Jacobian pattern (every rank builds
+    the same plan from the same seed, checkable by hash)."""
+    import hashlib
+
+    import numpy as np
+
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(indptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(indices, dtype=np.int64).tobytes())
+    return int.from_bytes(h.digest()[:8], "little") >> 1
+
+
+def check_same_pattern(indptr, indices, device="cpu", group=None) -> int:
+    """All ranks must hold the same pattern: min and max of the digest over
+    the group are compared; raises RuntimeError on a mismatch.  Returns the
+    digest.  (A NCCL group needs ``device`` to be the rank's GPU.)"""
+    import torch
+    import torch.distributed as dist
+
+    dg = pattern_digest(indptr, indices)
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return dg
+    lo = torch.tensor([dg], dtype=torch.int64, device=device)
+    hi = lo.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    if int(lo) != int(hi):
+        raise RuntimeError("ranks built different Jacobian patterns")
+    return dg
+
+
 def gather_norms(norms_local, K_local_max: int, group=None):
     """All-gather per-scenario infinity norms from every rank (blocking).
 

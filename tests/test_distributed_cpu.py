@@ -19,7 +19,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2011_11880_b200.batched import NormExchange, max_shard, shard
+from paper_2011_11880_b200.batched import (NormExchange, check_same_pattern, max_shard,
+                                           pattern_digest, shard)
 
 HERE = Path(__file__).resolve().parent
 
@@ -61,6 +62,7 @@ def _worker(rank, world, port, K, steps, q):
 
         s = _system()
         o = oracle.Oracle(s)
+        check_same_pattern(*o.pattern_csc())   # every rank built the same pattern
         lo, hi = shard(K, rank, world)
         nx = NormExchange(max_shard(K, world), "cpu")
         got = []
@@ -129,3 +131,34 @@ def test_sharded_norm_exchange(world, K):
         y, pq_p, pq_q, pv_p, out = _inputs(s, K, i, 0, K)
         _, _, ref = o.eval_scenarios(K, y, pq_p, pq_q, pv_p, out, want_g=False, want_j=False)
         assert np.array_equal(res[0][2][i], ref), i
+
+
+def _mismatch_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ptr = np.array([0, 1, 2], np.int32)
+        idx = np.array([0, rank], np.int32)     # rank 1 differs
+        try:
+            check_same_pattern(ptr, idx)
+            q.put((rank, "ok"))
+        except RuntimeError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pattern_check_detects_a_rank_with_another_pattern():
+    assert pattern_digest([0, 1], [0]) == pattern_digest(np.array([0, 1]), np.array([0]))
+    assert pattern_digest([0, 1], [0]) != pattern_digest([0, 1], [1])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_mismatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert all("different Jacobian patterns" in v for v in res.values()), res
