@@ -376,7 +376,7 @@ def batched_leg(args, workload: str, scaling: str, dev, rank: int, world: int,
 
         def host_step():
             plan.eval_batched_host(K, h_y, h_pqp, h_pqq, h_pvp, h_out, h_g, h_j, h_n,
-                                   blocks_per_stage=1, n_streams=4)
+                                   blocks_per_stage=1, n_streams=8)
 
         host_step()
     except Exception as e:  # noqa: BLE001
