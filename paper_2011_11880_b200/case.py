@@ -13,6 +13,7 @@ row indices) vectorised.
 
 from __future__ import annotations
 
+import re
 from dataclasses import dataclass
 
 import numpy as np
@@ -213,101 +214,125 @@ class CaseFormatError(ValueError):
 # minimum columns consumed per MATPOWER v2 matrix
 _MIN_COLS = {"bus": 10, "gen": 8, "branch": 11}
 
+# one assignment statement: "<lhs> = <rhs>" (lhs up to the first '=')
+_ASSIGNMENT = re.compile(r"^([^=]+?)\s*=\s*(.*?)\s*$")
+
+
+def _code_lines(text: str):
+    """(line number, code) of every line that holds code: '%' comments are
+    dropped, surrounding blanks stripped, empty lines skipped."""
+    for lineno, line in enumerate(text.splitlines(), start=1):
+        code = line.partition("%")[0].strip()
+        if code:
+            yield lineno, code
+
+
+class _Table:
+    """Rows of one matrix as they arrive.  A row ends at ';', at the end of a
+    line or at the closing ']'; text after ']' on that line is ignored."""
+
+    def __init__(self, key: str):
+        self.key = key
+        self.rows: list[list[float]] = []
+        self.lines: list[int] = []
+
+    def take(self, lineno: int, code: str) -> bool:
+        """Consume one line of the matrix body; True once it is closed."""
+        body, bracket, _ = code.partition("]")
+        for segment in body.split(";"):
+            toks = segment.split()
+            if toks:
+                self.rows.append(self._numbers(toks, lineno))
+                self.lines.append(lineno)
+        return bool(bracket)
+
+    def _numbers(self, toks: list[str], lineno: int) -> list[float]:
+        need = _MIN_COLS[self.key]
+        if len(toks) < need:
+            raise CaseFormatError(f"matrix {self.key!r} row has {len(toks)} columns, "
+                                  f"needs at least {need}", lineno)
+        out = []
+        for t in toks:
+            try:
+                out.append(float(t))
+            except ValueError:
+                raise CaseFormatError(f"non-numeric token {t!r} in matrix {self.key!r}",
+                                      lineno) from None
+        return out
+
+    def column(self, j: int, dtype=np.float64) -> np.ndarray:
+        return np.array([r[j] for r in self.rows], dtype=np.float64).astype(dtype)
+
 
 def parse_case(text: str, name: str = "") -> RawCase:
     """Parse the numeric-matrix subset of MATPOWER v2 case text.
 
     Accepts ``baseMVA`` and the ``bus``/``gen``/``branch`` assignments
     (``mpc.`` prefix optional), ``%`` comments, rows ended by ``;`` or a
-    newline.  Errors match pflow/case_io.py:85-158: malformed matrix,
-    non-numeric token, too few columns, missing baseMVA or matrix, matrix
-    assigned twice, duplicate bus id - each with its line number.  A tap
-    ratio of 0 becomes 1.0 (MATPOWER convention).
+    newline.  Other assignments (``version``, ``gencost``, ...) are skipped.
+    The error conditions and messages are pflow's (case_io.py:85-158, so a
+    caller's error handling carries over): malformed matrix, non-numeric
+    token, too few columns, missing baseMVA or matrix, matrix assigned twice,
+    duplicate bus id - each with its line number.  A tap ratio of 0 becomes
+    1.0 (MATPOWER convention).
     """
     base_mva = None
-    rows: dict[str, list[list[float]]] = {}
-    lines_of: dict[str, list[int]] = {}
-    current = None
-    lines = text.splitlines()
-    for lineno, raw in enumerate(lines, start=1):
-        body = raw.split("%", 1)[0].strip()
-        if not body:
+    tables: dict[str, _Table] = {}
+    open_table: _Table | None = None
+    for lineno, code in _code_lines(text):
+        if open_table is not None:
+            if open_table.take(lineno, code):
+                open_table = None
             continue
-        if current is None:
-            lhs, eq, rhs = body.partition("=")
-            if not eq:
-                continue
-            key = lhs.strip().split(".")[-1]
-            rhs = rhs.strip()
-            if key == "baseMVA":
-                try:
-                    base_mva = float(rhs.rstrip(";").strip())
-                except ValueError:
-                    raise CaseFormatError(f"baseMVA is not numeric: {rhs!r}", lineno) from None
-                continue
-            if key not in _MIN_COLS:
-                continue
-            if not rhs.startswith("["):
-                raise CaseFormatError(f"expected '[' to open matrix {key!r}", lineno)
-            if key in rows:
-                raise CaseFormatError(f"matrix {key!r} assigned twice", lineno)
-            rows[key], lines_of[key], current = [], [], key
-            body = rhs[1:]
-        closed = "]" in body
-        for seg in body.split("]", 1)[0].split(";"):
-            toks = seg.split()
-            if not toks:
-                continue
-            if len(toks) < _MIN_COLS[current]:
-                raise CaseFormatError(f"matrix {current!r} row has {len(toks)} columns, "
-                                      f"needs at least {_MIN_COLS[current]}", lineno)
+        m = _ASSIGNMENT.match(code)
+        if m is None:
+            continue                       # function header, other statements
+        key = m.group(1).rsplit(".", 1)[-1]
+        value = m.group(2)
+        if key == "baseMVA":
+            number = value.rstrip(";").strip()
             try:
-                rows[current].append([float(t) for t in toks])
+                base_mva = float(number)
             except ValueError:
-                bad = next(t for t in toks if not _is_float(t))
-                raise CaseFormatError(f"non-numeric token {bad!r} in matrix {current!r}",
-                                      lineno) from None
-            lines_of[current].append(lineno)
-        if closed:
-            current = None
-    if current is not None:
-        raise CaseFormatError(f"matrix {current!r} is never closed with '];'", len(lines))
+                raise CaseFormatError(f"baseMVA is not numeric: {number!r}", lineno) from None
+        elif key in _MIN_COLS:
+            if not value.startswith("["):
+                raise CaseFormatError(f"expected '[' to open matrix {key!r}", lineno)
+            if key in tables:
+                raise CaseFormatError(f"matrix {key!r} assigned twice", lineno)
+            open_table = tables[key] = _Table(key)
+            if open_table.take(lineno, value[1:]):
+                open_table = None
+    if open_table is not None:
+        raise CaseFormatError(f"matrix {open_table.key!r} is never closed with '];'",
+                              len(text.splitlines()))
     if base_mva is None:
         raise CaseFormatError("missing required scalar 'baseMVA'")
     for key in ("bus", "gen", "branch"):
-        if key not in rows:
+        if key not in tables:
             raise CaseFormatError(f"missing required matrix '{key}'")
-    seen: set[int] = set()
-    for r, ln in zip(rows["bus"], lines_of["bus"]):
-        bid = int(r[0])
-        if bid in seen:
-            raise CaseFormatError(f"duplicate bus id {bid}", ln)
-        seen.add(bid)
-
-    def col(key, j):
-        return np.array([r[j] for r in rows[key]], dtype=np.float64)
-
-    bus = {"bus_id": col("bus", 0).astype(np.int64), "bus_type": col("bus", 1).astype(np.int64),
-           "pd": col("bus", 2), "qd": col("bus", 3), "gs": col("bus", 4), "bs": col("bus", 5),
-           "vm": col("bus", 7), "va": col("bus", 8), "base_kv": col("bus", 9)}
-    gen = {"gen_bus": col("gen", 0).astype(np.int64), "pg": col("gen", 1), "qg": col("gen", 2),
-           "qmax": col("gen", 3), "qmin": col("gen", 4), "vg": col("gen", 5),
-           "gen_status": col("gen", 7).astype(np.int64)}
-    ratio = col("branch", 8)
-    branch = {"from_bus": col("branch", 0).astype(np.int64),
-              "to_bus": col("branch", 1).astype(np.int64), "r": col("branch", 2),
-              "x": col("branch", 3), "b": col("branch", 4),
-              "ratio": np.where(ratio != 0.0, ratio, 1.0), "angle": col("branch", 9),
-              "br_status": col("branch", 10).astype(np.int64)}
-    return make_case(base_mva, bus, gen, branch, name=name)
-
-
-def _is_float(tok: str) -> bool:
-    try:
-        float(tok)
-        return True
-    except ValueError:
-        return False
+    bus, gen, br = tables["bus"], tables["gen"], tables["branch"]
+    ids = bus.column(0, np.int64)
+    uniq, first, counts = np.unique(ids, return_index=True, return_counts=True)
+    if (counts > 1).any():   # report the first repeated row in file order
+        seen_first = np.zeros(ids.size, bool)
+        seen_first[first] = True
+        dup = int(np.flatnonzero(~seen_first)[0])
+        raise CaseFormatError(f"duplicate bus id {int(ids[dup])}", bus.lines[dup])
+    ratio = br.column(8)
+    return make_case(
+        base_mva,
+        {"bus_id": ids, "bus_type": bus.column(1, np.int64), "pd": bus.column(2),
+         "qd": bus.column(3), "gs": bus.column(4), "bs": bus.column(5), "vm": bus.column(7),
+         "va": bus.column(8), "base_kv": bus.column(9)},
+        {"gen_bus": gen.column(0, np.int64), "pg": gen.column(1), "qg": gen.column(2),
+         "qmax": gen.column(3), "qmin": gen.column(4), "vg": gen.column(5),
+         "gen_status": gen.column(7, np.int64)},
+        {"from_bus": br.column(0, np.int64), "to_bus": br.column(1, np.int64),
+         "r": br.column(2), "x": br.column(3), "b": br.column(4),
+         "ratio": np.where(ratio != 0.0, ratio, 1.0), "angle": br.column(9),
+         "br_status": br.column(10, np.int64)},
+        name=name)
 
 
 def parse_case_file(path) -> RawCase:
