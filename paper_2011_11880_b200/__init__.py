@@ -17,8 +17,6 @@ from .case import (CaseFormatError, RawCase, Violation, from_rows, make_case, pa
                    parse_case_file, validate_case, write_case)
 from .system_model import (AddressMap, LineGroup, PowerSystem, PqGroup, PvGroup, ShuntGroup,
                            SlackGroup, build_system, count_variables, flat_start, random_state)
-from .workflow import (WORKFLOW_TABLE, IntraStrategy, WorkflowConfig, WorkflowConfigError,
-                       all_workflows, set_worker_count, worker_count, workflow_config)
 
 __version__ = "0.1.0"
 
@@ -63,6 +61,5 @@ __all__ = [
     "from_rows", "gather_norms", "make_case", "newton_solve", "newton_solve_q_limits",
     "QLimitResult", "parse_case", "parse_case_file",
     "random_state", "shard", "symbolic_pattern", "validate_case", "write_case",
-    "SingularMatrixError", "SuperLUSolver", "WORKFLOW_TABLE", "IntraStrategy", "WorkflowConfig",
-    "WorkflowConfigError", "all_workflows", "set_worker_count", "worker_count", "workflow_config",
+    "SingularMatrixError", "SuperLUSolver",
 ]

@@ -24,7 +24,6 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from .plan import Plan
-from .workflow import WorkflowConfig, workflow_config
 
 _DIVERGENCE_LIMIT = 1e6   # pflow/newton.py:23
 
@@ -37,8 +36,10 @@ class SingularMatrixError(RuntimeError):
 class NewtonOptions:
     tol: float = 1e-8
     max_iter: int = 20
-    # accepted for pflow compatibility; the GPU path has one execution strategy
-    workflow: WorkflowConfig = field(default_factory=lambda: workflow_config(1))
+    # pflow's WorkflowConfig (newton.py:26-34) is accepted and ignored: the GPU
+    # path has one execution strategy, so pflow's CPU-workflow machinery
+    # (out of scope) is not reproduced
+    workflow: object = None
 
     def __post_init__(self):
         if self.tol <= 0:

@@ -833,7 +833,6 @@ def test_newton_driver_takes_pflow_style_solver_and_workspaces():
     from paper_2011_11880_b200.newton import NewtonOptions, newton_solve
     from paper_2011_11880_b200.residual import ResidualWorkspace
     from paper_2011_11880_b200.system_model import flat_start
-    from paper_2011_11880_b200.workflow import workflow_config
 
     class Solver:
         calls = 0
@@ -845,7 +844,7 @@ def test_newton_driver_takes_pflow_style_solver_and_workspaces():
     d = load("case14")
     s = system_of(d)
     plan = _plan(s)
-    res = newton_solve(s, flat_start(s), NewtonOptions(workflow=workflow_config(5)), Solver(),
+    res = newton_solve(s, flat_start(s), NewtonOptions(workflow="wf5, ignored"), Solver(),
                        residual_ws=ResidualWorkspace(s, plan), jacobian_ws=JacobianWorkspace(s, plan))
     assert res.converged and res.iterations == int(d["newton_iterations"])
     assert Solver.calls == res.iterations

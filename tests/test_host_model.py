@@ -119,31 +119,15 @@ def test_blocked_layout_roundtrip():
     assert flat[((65 // 32) * 5 + 3) * 32 + 65 % 32] == a[65, 3]
 
 
-def test_workflow_selection_surface_matches_pflow():
-    """pflow/workflow.py:44-107: same ids, table and validation errors (the
-    GPU path accepts the config and ignores it)."""
-    from paper_2011_11880_b200 import workflow as W
+def test_newton_options_accept_a_workflow_and_validate():
+    """pflow's NewtonOptions(workflow=...) is accepted (and ignored: one GPU
+    execution strategy); tol / max_iter are validated as pflow does."""
     from paper_2011_11880_b200.newton import NewtonOptions
 
-    assert W.WORKFLOW_TABLE == {1: ("serial", "serial"), 2: ("threaded", "serial"),
-                                3: ("serial", "threaded"), 4: ("threaded", "threaded"),
-                                5: ("serial", "simd"), 6: ("threaded", "simd")}
-    cfg = W.workflow_config(3, n_threads=4)
-    assert (cfg.id, cfg.inter, cfg.intra.kind, cfg.intra.n_threads) == (3, "serial", "threaded", 4)
-    assert W.workflow_config(5, n_threads=4).intra.n_threads == 1
-    assert [c.id for c in W.all_workflows(2)] == [1, 2, 3, 4, 5, 6]
-    for bad in (0, 7):
-        with pytest.raises(W.WorkflowConfigError):
-            W.workflow_config(bad)
-    with pytest.raises(W.WorkflowConfigError):
-        W.set_worker_count(0)
-    with pytest.raises(W.WorkflowConfigError):
-        W.IntraStrategy("gpu")
-    old = W.worker_count()
-    W.set_worker_count(3)
-    assert W.worker_count() == 3
-    W.set_worker_count(old)
-    assert NewtonOptions(workflow=W.workflow_config(6)).workflow.id == 6
+    marker = object()
+    assert NewtonOptions(workflow=marker).workflow is marker
+    with pytest.raises(ValueError):
+        NewtonOptions(max_iter=0)
     with pytest.raises(ValueError):
         NewtonOptions(tol=0)
 
