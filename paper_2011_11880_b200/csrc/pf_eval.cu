@@ -1287,8 +1287,12 @@ __device__ __forceinline__ void bulk_wait() {
 // the count.  (A memset of *norm before the launch plus a plain atomicMax
 // measured 2.5 us slower per evaluation inside a CUDA graph.)
 __device__ __forceinline__ void norm_post(unsigned long long nrm, unsigned long long* red) {
-    for (int o = 16; o > 0; o >>= 1) nrm = max(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    // warp max of a 64-bit value with two 32-bit reductions (REDUX): the
+    // high words first, then the low words of the lanes holding that high
+    const unsigned hi = (unsigned)(nrm >> 32);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)nrm : 0u);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ((unsigned long long)mh << 32) | ml;
 }
 __device__ __forceinline__ void norm_publish(const DevicePlan& d, const unsigned long long* red,
                                              unsigned long long* norm) {
