@@ -346,6 +346,7 @@ def batched_leg(args, workload: str, scaling: str, dev, rank: int, world: int,
             "config": workload_config(workload, sys_, plan.nnz),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_of(workload),
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
                          "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_launch,
                          "bytes_per_scenario": per_scen, "static_bytes": static,
                          "kernel_ms": kern_avg, "kernel_ms_max_over_ranks": kern_max,
