@@ -1030,3 +1030,55 @@ def test_q_limits_pv_to_pq_switching():
     rows_f = _pv_gen_rows(out.case)
     q_f = out.result.y[2 * sys_f.n_bus: 2 * sys_f.n_bus + len(rows_f)] * tight.base_mva
     assert np.all(q_f <= tight.qmax[rows_f] + 1e-9) and np.all(q_f >= tight.qmin[rows_f] - 1e-9)
+
+
+def test_extreme_states_bit_identical():
+    """States far from the power-flow operating range reach every sin/cos
+    branch of the glibc restatement inside the full evaluation: angle
+    differences up to ~60 rad (Cody-Waite reduction and the pi/2 - |x|
+    range), exactly zero differences (equal angles), differences below
+    2^-26 (x itself), and voltages down to 0 (exact-zero products).  Single
+    grid and scenario batch both bit-identical to wf1."""
+    from paper_2011_11880_b200.plan import from_blocked, to_blocked
+
+    s = build_system(synth.synth_case(400, 560, seed=11, pq_frac=0.6, pv_frac=0.15,
+                                      shunt_frac=0.1, shift_frac=0.2, hub_frac=0.02,
+                                      hub_degree=20))
+    plan = _plan(s)
+    o = oracle.Oracle(s)
+    _, _, perm = plan.pattern_csc()
+    rng = np.random.default_rng(5)
+    nb = s.n_bus
+    base = random_state(s, 3)
+    states = []
+    y = base.copy()
+    y[:nb] = rng.uniform(-30.0, 30.0, nb)
+    y[nb:2 * nb] = rng.uniform(0.5, 1.5, nb)
+    states.append(y)                                    # reduction / mid ranges
+    y = base.copy()
+    y[:nb] = 0.3
+    states.append(y)                                    # equal angles: d = 0
+    y = base.copy()
+    y[:nb] = 0.1 + 1e-10 * rng.standard_normal(nb)
+    states.append(y)                                    # |d| < 2^-26
+    y = base.copy()
+    y[:nb] = rng.normal(0.0, 1.0, nb)
+    y[nb:2 * nb] = np.where(rng.random(nb) < 0.1, 0.0, y[nb:2 * nb])
+    states.append(y)                                    # V = 0 on 10 % of buses
+    for k, y in enumerate(states):
+        g, j, n = _eval(plan, y)
+        assert_parity(g, o.residual(y), f"state {k} g")
+        assert_parity(j[perm], o.jacobian(y), f"state {k} J")
+        assert n == np.abs(g).max()
+    K = len(states)
+    ys = np.stack(states)
+    gb, jb, nrm = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K), plan.empty(K)
+    plan.eval_batched(K, _dev(to_blocked(ys)), g=gb, jval=jb, norms=nrm)
+    torch.cuda.synchronize()
+    G = from_blocked(gb.cpu().numpy(), K, plan.n_var)
+    J = from_blocked(jb.cpu().numpy(), K, plan.nnz)
+    for k, y in enumerate(states):
+        g1, j1, n1 = _eval(plan, y)
+        assert np.array_equal(G[k].view(np.int64), g1.view(np.int64)), k
+        assert np.array_equal(J[k].view(np.int64), j1.view(np.int64)), k
+        assert float(nrm[k]) == n1
