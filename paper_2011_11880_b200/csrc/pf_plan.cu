@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
 #include <string>
@@ -390,6 +391,22 @@ int validate(const pf_topology* t) {
     return PF_OK;
 }
 
+// Processing order of the batched kernels' ordinary buses: the spanning-tree
+// preorder or the bus order.  The preorder removes most re-reads of
+// neighbour state rows (ncu, DRAM reads per launch: config 3 805 -> 684 MB,
+// config 4 881 -> 719 MB) but turns the sequential first reads of a bus's own
+// rows into random 256-byte reads, so it pays only when one 32-scenario
+// block's state rows crowd L2 (B200: config 4, 110 MB of rows, 0.537 ->
+// 0.530 ms; config 3, 37 MB, 0.575 -> 0.584 ms).  PF_ORDER=tree|bus forces
+// one (read once per process).
+static bool tree_order(int64_t n_var) {
+    static const int v = [] {
+        const char* e = getenv("PF_ORDER");
+        return !e ? 0 : std::strcmp(e, "bus") == 0 ? 1 : std::strcmp(e, "tree") == 0 ? 2 : 0;
+    }();
+    return v ? v == 2 : n_var * PF_LANES * 8 > (64ll << 20);
+}
+
 #define PF_TRY(call)                                               \
     do {                                                           \
         cudaError_t _e = (call);                                   \
@@ -644,8 +661,61 @@ int build(const pf_topology* t, pf_plan** out) {
             taken[slot] = 1;
             order[slot] = hubs[h];
         }
+        // Buses of ordinary degree fill the remaining slots in bus order or
+        // (tree_order) in the preorder of a breadth-first spanning forest whose
+        // children are visited smallest subtree first.  At any time
+        // the kernel works on a window of G WS_W consecutive slots, so a
+        // bus's state rows are in L2 for a neighbour's item when the two
+        // slots are close; in this order a tree branch (N - 1 of the
+        // branches of a connected grid) is 1 + the smaller siblings'
+        // subtrees apart.
+        std::vector<int32_t> seq;
+        seq.reserve(N);
+        if (tree_order(d.n_var)) {
+            std::vector<int4> hm(n_inc);
+            if (n_inc)
+                PF_TRY(cudaMemcpy(hm.data(), d.inc_meta, sizeof(int4) * (size_t)n_inc,
+                                  cudaMemcpyDeviceToHost));
+            std::vector<int32_t> par(N, -2), bfs, sz(N, 1), cptr(N + 2, 0), kids(N);
+            bfs.reserve(N);
+            for (int32_t r = 0; r < N; ++r) {
+                if (par[r] != -2) continue;
+                par[r] = -1;
+                bfs.push_back(r);
+                for (size_t q = bfs.size() - 1; q < bfs.size(); ++q) {
+                    const int32_t u = bfs[q];
+                    for (int32_t e = hptr[u]; e < hptr[u + 1]; ++e) {
+                        const int32_t v = hm[e].x;
+                        if (v < 0 || v >= N || par[v] != -2) continue;
+                        par[v] = u;
+                        bfs.push_back(v);
+                    }
+                }
+            }
+            for (int64_t q = N - 1; q >= 0; --q)
+                if (par[bfs[q]] >= 0) sz[par[bfs[q]]] += sz[bfs[q]];
+            for (int32_t v = 0; v < N; ++v) cptr[(par[v] >= 0 ? par[v] : N) + 1]++;
+            for (int32_t u = 0; u <= N; ++u) cptr[u + 1] += cptr[u];
+            {
+                std::vector<int32_t> cur(cptr.begin(), cptr.end() - 1);
+                for (int32_t v = 0; v < N; ++v) kids[cur[par[v] >= 0 ? par[v] : N]++] = v;
+            }
+            // cptr[u] .. cptr[u + 1]: children of u (u = N: the roots), by bus
+            for (int32_t u = 0; u < N; ++u)
+                std::stable_sort(kids.begin() + cptr[u], kids.begin() + cptr[u + 1],
+                                 [&](int32_t a, int32_t b) { return sz[a] < sz[b]; });
+            std::vector<int32_t> stack(kids.rbegin(), kids.rbegin() + (cptr[N + 1] - cptr[N]));   // roots
+            while (!stack.empty()) {
+                const int32_t u = stack.back();
+                stack.pop_back();
+                seq.push_back(u);
+                for (int32_t c = cptr[u + 1]; c-- > cptr[u];) stack.push_back(kids[c]);
+            }
+        } else {
+            for (int32_t i = 0; i < N; ++i) seq.push_back(i);
+        }
         int32_t next = 0;
-        for (int32_t i = 0; i < N; ++i) {
+        for (const int32_t i : seq) {
             if (hptr[i + 1] - hptr[i] >= HUB_DEG) continue;
             while (taken[next]) ++next;
             taken[next] = 1;

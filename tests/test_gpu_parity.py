@@ -897,8 +897,9 @@ def test_previous_batched_kernel_still_matches(tmp_path):
     """PF_BATCHED_KERNEL=old selects the previous single-role batched kernel
     (kept for A/B timing, scripts/ab_env.sh), PF_SCHEDULE forces the staged
     kernel's static or dynamic schedule, PF_STAGING=tma its TMA gather4
-    staging; in fresh processes every variant must give the same bits as the
-    default."""
+    staging, PF_ORDER the processing order of the buses (spanning-tree
+    preorder or bus order; the default picks by grid size); in fresh processes
+    every variant must give the same bits as the default."""
     import subprocess
     import sys
 
@@ -927,10 +928,12 @@ np.savez(sys.argv[2], g=g.cpu().numpy(), j=j.cpu().numpy(), n=n.cpu().numpy())
     runs = {"staged": {}, "old": {"PF_BATCHED_KERNEL": "old"},
             "static": {"PF_SCHEDULE": "static"}, "dynamic": {"PF_SCHEDULE": "dynamic"},
             "tma_static": {"PF_STAGING": "tma", "PF_SCHEDULE": "static"},
-            "tma_dynamic": {"PF_STAGING": "tma", "PF_SCHEDULE": "dynamic"}}
+            "tma_dynamic": {"PF_STAGING": "tma", "PF_SCHEDULE": "dynamic"},
+            "tree_order": {"PF_ORDER": "tree"}, "bus_order": {"PF_ORDER": "bus"},
+            "tree_old": {"PF_ORDER": "tree", "PF_BATCHED_KERNEL": "old"}}
     for kind, extra in runs.items():
         env = dict(os.environ)
-        for v in ("PF_BATCHED_KERNEL", "PF_SCHEDULE", "PF_STAGING"):
+        for v in ("PF_BATCHED_KERNEL", "PF_SCHEDULE", "PF_STAGING", "PF_ORDER"):
             env.pop(v, None)
         env.update(extra)
         f = tmp_path / f"{kind}.npz"
