@@ -702,8 +702,11 @@ int build(const pf_topology* t, pf_plan** out) {
             }
             // cptr[u] .. cptr[u + 1]: children of u (u = N: the roots), by bus
             for (int32_t u = 0; u < N; ++u)
-                std::stable_sort(kids.begin() + cptr[u], kids.begin() + cptr[u + 1],
-                                 [&](int32_t a, int32_t b) { return sz[a] < sz[b]; });
+                if (cptr[u + 1] - cptr[u] > 1)   // (ties by bus: deterministic)
+                    std::sort(kids.begin() + cptr[u], kids.begin() + cptr[u + 1],
+                              [&](int32_t a, int32_t b) {
+                                  return sz[a] != sz[b] ? sz[a] < sz[b] : a < b;
+                              });
             std::vector<int32_t> stack(kids.rbegin(), kids.rbegin() + (cptr[N + 1] - cptr[N]));   // roots
             while (!stack.empty()) {
                 const int32_t u = stack.back();
