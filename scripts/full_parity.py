@@ -24,7 +24,7 @@ for wl in sys.argv[1:] or ["config3", "config4"]:
     s = bench.build_case(wl)
     plan = Plan(s)
     _, _, perm = plan.pattern_csc()
-    y, pq_p, pq_q, pv_p, out = bench.blocked_inputs(s, K, 1000)
+    y, pq_p, pq_q, pv_p, out = bench.blocked_inputs(s, K, int(os.environ.get("SEED", "1000")))
     t = lambda a: torch.from_numpy(a).cuda()
     g, j, n = plan.empty(plan.n_var, K), plan.empty(plan.nnz, K), plan.empty(K)
     plan.eval_batched(K, t(y), t(pq_p), t(pq_q), t(pv_p), t(out), g, j, n)
