@@ -1092,9 +1092,12 @@ __global__ void __launch_bounds__(32 * W, MINB) k_eval_staged(
             const uint32_t sbu = slots_u32 + (k & 1) * WS_SLOT_BYTES;
             const StagedSrc src{{d, A, A.y + lane, cnt.z, lane}, sbu + lane * 8,
                                 sbu + WS_ROWS * WS_ROW_BYTES, cnt.x, cnt.y};
-            nrm = max(nrm, eval_bus_src<MODE, PF_LANES>(
-                               d, tab, cnt.z, src, A, lane, out_l,
-                               GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk));
+            // (the running max is read from shared memory after the bus, not
+            // held in registers through it)
+            const unsigned long long r = eval_bus_src<MODE, PF_LANES>(
+                d, tab, cnt.z, src, A, lane, out_l,
+                GlobalJ<PF_LANES>{A.j ? A.j + lane : nullptr}, ochk);
+            nrm = max(nrm, r);
         }
         __syncwarp();         // slot reads done before it is refilled
     };
