@@ -678,15 +678,20 @@ int build(const pf_topology* t, pf_plan** out) {
                                   cudaMemcpyDeviceToHost));
             std::vector<int32_t> par(N, -2), bfs, sz(N, 1), cptr(N + 2, 0), kids(N);
             bfs.reserve(N);
+            // (the forest does not pass through hubs: they are placed in the
+            // first rounds whatever their rank, so a bus adopted by a hub would
+            // lose the one neighbour that can be near it)
+            auto is_hub = [&](int32_t i) { return hptr[i + 1] - hptr[i] >= HUB_DEG; };
             for (int32_t r = 0; r < N; ++r) {
                 if (par[r] != -2) continue;
                 par[r] = -1;
                 bfs.push_back(r);
+                if (is_hub(r)) continue;
                 for (size_t q = bfs.size() - 1; q < bfs.size(); ++q) {
                     const int32_t u = bfs[q];
                     for (int32_t e = hptr[u]; e < hptr[u + 1]; ++e) {
                         const int32_t v = hm[e].x;
-                        if (v < 0 || v >= N || par[v] != -2) continue;
+                        if (v < 0 || v >= N || par[v] != -2 || is_hub(v)) continue;
                         par[v] = u;
                         bfs.push_back(v);
                     }
