@@ -4,14 +4,14 @@
 # bench arms, the config-4 bench line and the launch list.
 set -x
 if [ "$1" = ncu ]; then
-python -m pytest tests -m gpu -x -q > gpurun_out/r02i_pytest.log 2>&1; tail -2 gpurun_out/r02i_pytest.log
-REPS=3 ncu --set full --clock-control none --import-source on -k regex:k_eval_staged -s 3 -c 1 -f -o gpurun_out/r02i_c3 python scripts/kbench.py > gpurun_out/r02i_ncu_c3.log 2>&1
-WORKLOAD=config4 REPS=3 ncu --set full --clock-control none --import-source on -k regex:k_eval_staged -s 3 -c 1 -f -o gpurun_out/r02i_c4 python scripts/kbench.py > gpurun_out/r02i_ncu_c4.log 2>&1
+python -m pytest tests -m gpu -x -q > gpurun_out/r02j_pytest.log 2>&1; tail -2 gpurun_out/r02j_pytest.log
+REPS=3 ncu --set full --clock-control none --import-source on -k regex:k_eval_staged -s 3 -c 1 -f -o gpurun_out/r02j_c3 python scripts/kbench.py > gpurun_out/r02j_ncu_c3.log 2>&1
+WORKLOAD=config4 REPS=3 ncu --set full --clock-control none --import-source on -k regex:k_eval_staged -s 3 -c 1 -f -o gpurun_out/r02j_c4 python scripts/kbench.py > gpurun_out/r02j_ncu_c4.log 2>&1
 else
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02i_smoke.log 2>&1; tail -1 gpurun_out/r02i_smoke.log
-python bench.py --impl reference > gpurun_out/r02i_reference.json 2> gpurun_out/r02i_reference.err
-python bench.py > gpurun_out/r02i_bench.json 2> gpurun_out/r02i_bench.err
-python bench.py --workload config4 --no-single > gpurun_out/r02i_bench_c4.json 2> gpurun_out/r02i_bench_c4.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02i_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-single > gpurun_out/r02i_launches.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02j_smoke.log 2>&1; tail -1 gpurun_out/r02j_smoke.log
+python bench.py --impl reference > gpurun_out/r02j_reference.json 2> gpurun_out/r02j_reference.err
+python bench.py > gpurun_out/r02j_bench.json 2> gpurun_out/r02j_bench.err
+python bench.py --workload config4 --no-single > gpurun_out/r02j_bench_c4.json 2> gpurun_out/r02j_bench_c4.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02j_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-single > gpurun_out/r02j_launches.log 2>&1
 fi
-ls -la gpurun_out/r02i*
+ls -la gpurun_out/r02j*
