@@ -391,14 +391,14 @@ int validate(const pf_topology* t) {
     return PF_OK;
 }
 
-// Processing order of the batched kernels' ordinary buses: the spanning-tree
-// preorder or the bus order.  The preorder removes most re-reads of
-// neighbour state rows (ncu, DRAM reads per launch: config 3 805 -> 684 MB,
-// config 4 881 -> 719 MB) but turns the sequential first reads of a bus's own
-// rows into random 256-byte reads, so it pays only when one 32-scenario
-// block's state rows crowd L2 (B200: config 4, 110 MB of rows, 0.537 ->
-// 0.530 ms; config 3, 37 MB, 0.575 -> 0.584 ms).  PF_ORDER=tree|bus forces
-// one (read once per process).
+// Processing order of the batched kernels' ordinary buses: the preorder of a
+// spanning forest or the bus order.  The preorder removes most re-reads of
+// neighbour state rows (ncu, DRAM reads per launch: config 3 804 -> 683 MB,
+// config 4 879 -> 633 MB) but turns the sequential first reads of a bus's own
+// rows into random 256-byte reads, so it pays where one 32-scenario block's
+// state rows crowd L2 (B200: config 4, 110 MB of rows, 0.535-0.538 ->
+// 0.512-0.513 ms) and not where they fit well (config 3, 37 MB: 0.570-0.574
+// -> 0.575-0.576 ms).  PF_ORDER=tree|bus forces one (read once per process).
 static bool tree_order(int64_t n_var) {
     static const int v = [] {
         const char* e = getenv("PF_ORDER");
